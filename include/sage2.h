@@ -1,0 +1,132 @@
+/*
+ * sage2.h -- C ABI of libsage2.so: the SageAttention2 (arXiv 2411.10958) quantized attention
+ * forward pass, B200 (sm_100a) native.
+ *
+ * Citations: P:N = PAPER.md line N (the paper's LaTeX); DESIGN.md holds the readings (C-n).
+ *
+ * What it computes (Fig. 3; Alg. 1), per (batch b, query head h):
+ *   1. smooth K:  gamma(K) = K - mean_tokens(K)
+ *      smooth Q:  gamma(Q_i) = Q_i - mean(Q_i) per 128-token block i
+ *      Delta S_i = q_bar_i gamma(K)^T
+ *   2. per-thread INT4 quantization of gamma(Q), gamma(K) (groups of P:223),
+ *      per-channel FP8 E4M3 quantization of V
+ *   3. S = (psi^-1(Q^ K^T) + Delta S)/sqrt(d), exact INT32 QK^T on tcgen05 kind::i8 (INT4 values
+ *      in int8 lanes: sm_100a has no dense INT4 tensor-core MMA), online softmax, P~ -> E4M3 with
+ *      the static scale 448, R_j = P^ V^ on tcgen05 kind::f8f6f4 in a fresh
+ *      accumulator, O = diag(exp(m_old - m_new)) O + R_j in FP32 (two-level accumulation,
+ *      P:258), O = O / l / 448 * delta_V.
+ *   softmax scale 1/sqrt(d); causal = key <= query; GQA: query head h uses KV head
+ *   h / (H_q / H_kv).
+ *
+ * Layouts (all contiguous, row-major):
+ *   q   [B, H_q,  N, d] fp16      k, v [B, H_kv, N, d] fp16      out [B, H_q, N, d] fp16
+ * d in {64, 128}; N >= 1 (ragged N allowed); H_q % H_kv == 0.
+ *
+ * Ownership: every pointer is caller-owned.  Device pointers must be 16-byte aligned device
+ * memory of the current CUDA device.  The library never frees caller memory and keeps no state
+ * between calls except cached kernel attributes.
+ *
+ * Errors: functions return SAGE2_OK (0) or a negative code; nothing is printed and no C++
+ * exception crosses the ABI.  Work is enqueued asynchronously on `stream` (a cudaStream_t, NULL =
+ * legacy default stream); device-side faults surface at the caller's next synchronization.
+ * There is no CPU fallback: on a device that is not sm_100 every entry point returns
+ * SAGE2_EUNSUPPORTED.
+ */
+#ifndef SAGE2_H_
+#define SAGE2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAGE2_OK 0
+#define SAGE2_EINVAL (-1)       /* bad shape / null or misaligned pointer / workspace too small */
+#define SAGE2_EUNSUPPORTED (-2) /* current device is not sm_100 (B200)                          */
+#define SAGE2_ENOMEM (-3)       /* stream-ordered workspace allocation failed                    */
+#define SAGE2_ECUDA (-4)        /* a CUDA launch / API call failed (cudaGetLastError)            */
+
+/* Variant flags (bitwise OR) for the *_ex entry points. */
+#define SAGE2_F_CAUSAL 1   /* key <= query mask                                                  */
+#define SAGE2_F_INT8 2     /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing,  */
+                           /* P:70, P:476 (Table 3)                                    */
+
+/* Library version (monotone integer). */
+int sage2_version(void);
+
+/* Human-readable name of an error code (static string). */
+const char* sage2_strerror(int code);
+
+/* Bytes of device workspace sage2_attn_ws needs for this problem: Q^/K^/V^ tile images, scales,
+ * q_bar/k_bar, and Delta S (4 * B * H_q * (N_pad/128) * N_pad bytes, the dominant term;
+ * N_pad = ceil(N/128)*128).  Returns 0 for invalid shapes. */
+size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int causal);
+
+/* Full forward pass (preprocessing + attention kernel).  Allocates its workspace stream-ordered
+ * (cudaMallocAsync / cudaFreeAsync on `stream`).  causal: 0 or 1. */
+int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N,
+               int d, int causal, void* stream);
+
+/* Same, with a caller-provided device workspace of at least sage2_workspace_bytes(...) bytes
+ * (256-byte aligned).  No allocation happens inside. */
+int sage2_attn_ws(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N,
+                  int d, int causal, void* workspace, size_t ws_bytes, void* stream);
+
+/* Same as sage2_attn_ws with variant flags (SAGE2_F_*). */
+int sage2_attn_ex(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N,
+                  int d, int flags, void* workspace, size_t ws_bytes, void* stream);
+
+/* End-to-end call on HOST buffers (page-locked memory recommended; same layouts as above):
+ * allocates device copies and the workspace stream-ordered, copies q/k/v host->device, runs the
+ * forward pass, copies out device->host, frees.  Asynchronous on `stream` like every other entry
+ * point: the caller synchronizes `stream` before reading out. */
+int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, void* out_host, int B, int H_q,
+                    int H_kv, int N, int d, int causal, void* stream);
+
+/* ---- staged entry points (the same kernels, split so each stage can be timed / inspected) ---- */
+
+/* Workspace layout: writes SAGE2_WS_NREGIONS byte offsets into offsets[] (regions in order:
+ * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]),
+ * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][N_pad/4]), qbar(f32 [B*H_q][nT][d]),
+ * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][N_pad/16]),
+ * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), ds(f32 [B*H_q][nT][N_pad], scaled by
+ * log2(e)/sqrt(d)), end) -- tile images are K-major, 128B (d=128) / 64B (d=64) swizzled, the exact
+ * shared-memory image the tensor cores read.  Returns 0 or SAGE2_EINVAL. */
+#define SAGE2_WS_NREGIONS 12
+int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
+
+/* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */
+int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
+                  int flags, void* workspace, size_t ws_bytes, void* stream);
+
+/* Attention kernel only (Fig. 3 step 4), on a workspace filled by sage2_prepare with the same
+ * shapes and flags. */
+int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
+                    size_t ws_bytes, void* stream);
+
+/* Debug: runs the attention kernel non-causally and additionally writes the raw INT32 QK^T
+ * accumulators read back from TMEM to s_int [B*H_q][N_pad][N_pad] (device, caller-owned,
+ * 4*B*H_q*N_pad^2 bytes; intended for small N).  out receives the normal output. */
+int sage2_debug_qk_int32(void* out, int32_t* s_int, int B, int H_q, int H_kv, int N, int d, int flags,
+                         const void* workspace, size_t ws_bytes, void* stream);
+
+/* Probe (the experiment of P:284-285 repeated on tcgen05).  For each of n
+ * fp32 bit patterns D[i] (host array) the accumulator of tcgen05.mma.kind::f8f6f4 (M=128, N=32,
+ * K=32, E4M3 x E4M3 -> F32) is initialised to D[i] and one MMA with enable-input-d is issued:
+ *   c_zero[i] = bits of (A B + D) with A = B = 0                       (the paper's test)
+ *   c_prod[i] = bits of (x[i] * 1.0 + D[i]), x[i] = E4M3 value of prod_vals[i] (one non-zero product)
+ * Host arrays, synchronous.  Returns 0 or an error code. */
+int sage2_probe_accumulator(const uint32_t* d_bits, const uint8_t* prod_vals, int n, uint32_t* c_zero,
+                            uint32_t* c_prod);
+
+/* Microbenchmark: issues `iters` back-to-back tcgen05.mma of the given kind (0 = i8 M128 N256 K32,
+ * 1 = f8f6f4 E4M3 M128 N256 K32) on every SM and returns the measured dense ops/s in *ops_per_s.
+ * Synchronous. */
+int sage2_bench_mma(int kind, int iters, double* ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGE2_H_ */

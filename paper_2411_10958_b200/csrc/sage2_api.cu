@@ -1,0 +1,302 @@
+// sage2_api.cu -- the C ABI of libsage2.so (include/sage2.h): validation, workspace layout,
+// stream-ordered launches of the preprocessing kernels (prep.cuh) and the tcgen05 attention
+// kernel (attn.cuh), plus the accumulator probe and the tensor-core microbenchmark (probe.cuh).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/sage2.h"
+#include "attn.cuh"
+#include "prep.cuh"
+#include "probe.cuh"
+
+using namespace sage2;
+
+namespace {
+
+constexpr int kVersion = 1;
+
+int check_device() {
+    static int state = 0;   // 0 unknown, 1 ok, -1 unsupported
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return SAGE2_ECUDA;
+    static int cached_dev = -1;
+    if (state == 0 || cached_dev != dev) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+            return SAGE2_ECUDA;
+        state = (major == 10 && minor == 0) ? 1 : -1;
+        cached_dev = dev;
+    }
+    return state == 1 ? SAGE2_OK : SAGE2_EUNSUPPORTED;
+}
+
+bool shapes_ok(int B, int Hq, int Hkv, int N, int d) {
+    return B >= 1 && Hq >= 1 && Hkv >= 1 && N >= 1 && (d == 64 || d == 128) && Hq % Hkv == 0 &&
+           N <= (1 << 22);
+}
+
+struct Layout {
+    size_t off[SAGE2_WS_NREGIONS];
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
+    const size_t nT = (size_t)(N + 127) / 128, Np = nT * 128;
+    const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
+    const size_t sizes[SAGE2_WS_NREGIONS - 1] = {
+        BHk * d * 8,          // ksum
+        BHk * d * 4,          // vmax
+        BHk * d * 4,          // kbar
+        BHk * d * 4,          // dv
+        BHq * Np * d,         // qhat
+        BHq * (Np / 4) * 4,   // dq
+        BHq * nT * d * 4,     // qbar
+        BHk * Np * d,         // khat
+        BHk * (Np / 16) * 4,  // dk
+        BHk * Np * d,         // vhat
+        BHq * nT * Np * 4,    // ds
+    };
+    Layout L;
+    size_t o = 0;
+    for (int r = 0; r < SAGE2_WS_NREGIONS - 1; ++r) {
+        L.off[r] = o;
+        o = align_up(o + sizes[r], 1024);
+    }
+    L.off[SAGE2_WS_NREGIONS - 1] = o;
+    return L;
+}
+
+enum { R_KSUM, R_VMAX, R_KBAR, R_DV, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_END };
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int D>
+int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int Hq, int Hkv, int N, int flags,
+                   uint8_t* ws, const Layout& L, cudaStream_t st) {
+    const int nT = (N + 127) / 128;
+    const int qk_max = (flags & SAGE2_F_INT8) ? 127 : 7;
+    const int smooth_q = (flags & SAGE2_F_INT8) ? 0 : 1;   // SageAttn2-8b: no Q smoothing
+    const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
+    if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return SAGE2_ECUDA;
+    auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
+    auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
+    const int rows_per_cta = 512;
+    k_kv_stats<D><<<dim3((N + rows_per_cta - 1) / rows_per_cta, BHk), 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax);
+    k_kv_quant<D><<<dim3(nT, BHk), 256, 0, st>>>(
+        k, v, N, qk_max, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
+        reinterpret_cast<float*>(ws + L.off[R_DK]), ws + L.off[R_VHAT], reinterpret_cast<float*>(ws + L.off[R_KBAR]),
+        reinterpret_cast<float*>(ws + L.off[R_DV]));
+    k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
+                                                reinterpret_cast<float*>(ws + L.off[R_DQ]),
+                                                reinterpret_cast<float*>(ws + L.off[R_QBAR]));
+    const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
+                                                reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
+                                                scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]));
+    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+}
+
+template <int D, bool CAUSAL, bool DUMP>
+int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = AttnSmem<D>;
+    // D=64 needs less shared memory; request enough to keep one CTA per SM (TMEM: 512 columns).
+    constexpr uint32_t smem = L::ALLOC > 120 * 1024 ? L::ALLOC : 120 * 1024;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return SAGE2_ECUDA;
+        configured = true;
+    }
+    k_attn<D, CAUSAL, DUMP><<<dim3(p.nT, p.Hq, B), 192, smem, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+}
+
+int launch_attention(void* out, int32_t* s_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
+                     const Layout& L, cudaStream_t st) {
+    AttnParams p;
+    p.qhat = reinterpret_cast<const int8_t*>(ws + L.off[R_QHAT]);
+    p.dq = reinterpret_cast<const float*>(ws + L.off[R_DQ]);
+    p.khat = reinterpret_cast<const int8_t*>(ws + L.off[R_KHAT]);
+    p.dk = reinterpret_cast<const float*>(ws + L.off[R_DK]);
+    p.vhat = ws + L.off[R_VHAT];
+    p.dv = reinterpret_cast<const float*>(ws + L.off[R_DV]);
+    p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
+    p.out = reinterpret_cast<__half*>(out);
+    p.s_dump = s_dump;
+    p.Hq = Hq;
+    p.Hkv = Hkv;
+    p.N = N;
+    p.nT = (N + 127) / 128;
+    p.qk_scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+    const bool causal = (flags & SAGE2_F_CAUSAL) != 0;
+    if (s_dump) {
+        if (d == 64) return launch_attn_t<64, false, true>(p, B, st);
+        return launch_attn_t<128, false, true>(p, B, st);
+    }
+    if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
+    return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
+}
+
+int validate(const void* q, const void* k, const void* v, const void* out, int B, int Hq, int Hkv, int N, int d) {
+    if (!shapes_ok(B, Hq, Hkv, N, d)) return SAGE2_EINVAL;
+    if (!q || !k || !v || !out) return SAGE2_EINVAL;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out)) return SAGE2_EINVAL;
+    return SAGE2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sage2_version(void) { return kVersion; }
+
+const char* sage2_strerror(int code) {
+    switch (code) {
+        case SAGE2_OK: return "ok";
+        case SAGE2_EINVAL: return "invalid argument (shape, pointer, alignment or workspace size)";
+        case SAGE2_EUNSUPPORTED: return "unsupported device: libsage2 requires sm_100 (B200)";
+        case SAGE2_ENOMEM: return "workspace allocation failed";
+        case SAGE2_ECUDA: return "CUDA error";
+        default: return "unknown error";
+    }
+}
+
+size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int /*causal*/) {
+    if (!shapes_ok(B, H_q, H_kv, N, d)) return 0;
+    return make_layout(B, H_q, H_kv, N, d).off[R_END];
+}
+
+int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets) {
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !offsets) return SAGE2_EINVAL;
+    Layout L = make_layout(B, H_q, H_kv, N, d);
+    std::memcpy(offsets, L.off, sizeof(L.off));
+    return SAGE2_OK;
+}
+
+int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d, int flags,
+                  void* workspace, size_t ws_bytes, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !q || !k || !v || !workspace) return SAGE2_EINVAL;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (reinterpret_cast<uintptr_t>(workspace) & 255)) return SAGE2_EINVAL;
+    Layout L = make_layout(B, H_q, H_kv, N, d);
+    if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto* ws = reinterpret_cast<uint8_t*>(workspace);
+    auto* hq = reinterpret_cast<const __half*>(q);
+    auto* hk = reinterpret_cast<const __half*>(k);
+    auto* hv = reinterpret_cast<const __half*>(v);
+    return d == 64 ? launch_prepare<64>(hq, hk, hv, B, H_q, H_kv, N, flags, ws, L, st)
+                   : launch_prepare<128>(hq, hk, hv, B, H_q, H_kv, N, flags, ws, L, st);
+}
+
+int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
+                    size_t ws_bytes, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out)) return SAGE2_EINVAL;
+    Layout L = make_layout(B, H_q, H_kv, N, d);
+    if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
+    return launch_attention(out, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sage2_debug_qk_int32(void* out, int32_t* s_int, int B, int H_q, int H_kv, int N, int d, int flags,
+                         const void* workspace, size_t ws_bytes, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace) return SAGE2_EINVAL;
+    Layout L = make_layout(B, H_q, H_kv, N, d);
+    if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
+    return launch_attention(out, s_int, B, H_q, H_kv, N, d, flags & ~SAGE2_F_CAUSAL,
+                            reinterpret_cast<const uint8_t*>(workspace), L, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sage2_attn_ex(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N, int d,
+                  int flags, void* workspace, size_t ws_bytes, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    rc = validate(q, k, v, out, B, H_q, H_kv, N, d);
+    if (rc) return rc;
+    rc = sage2_prepare(q, k, v, B, H_q, H_kv, N, d, flags, workspace, ws_bytes, stream);
+    if (rc) return rc;
+    return sage2_attention(out, B, H_q, H_kv, N, d, flags, workspace, ws_bytes, stream);
+}
+
+int sage2_attn_ws(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N, int d,
+                  int causal, void* workspace, size_t ws_bytes, void* stream) {
+    return sage2_attn_ex(q, k, v, out, B, H_q, H_kv, N, d, causal ? SAGE2_F_CAUSAL : 0, workspace, ws_bytes, stream);
+}
+
+int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N, int d,
+               int causal, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    rc = validate(q, k, v, out, B, H_q, H_kv, N, d);
+    if (rc) return rc;
+    const size_t bytes = sage2_workspace_bytes(B, H_q, H_kv, N, d, causal);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    void* ws = nullptr;
+    if (cudaMallocAsync(&ws, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return SAGE2_ENOMEM;
+    }
+    rc = sage2_attn_ws(q, k, v, out, B, H_q, H_kv, N, d, causal, ws, bytes, stream);
+    if (cudaFreeAsync(ws, st) != cudaSuccess && rc == SAGE2_OK) rc = SAGE2_ECUDA;
+    return rc;
+}
+
+int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, void* out_host, int B, int H_q,
+                    int H_kv, int N, int d, int causal, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !q_host || !k_host || !v_host || !out_host) return SAGE2_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t qb = (size_t)B * H_q * N * d * 2, kb = (size_t)B * H_kv * N * d * 2;
+    const size_t wsb = sage2_workspace_bytes(B, H_q, H_kv, N, d, causal);
+    void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *ws = nullptr;
+    if (cudaMallocAsync(&dq, qb, st) != cudaSuccess || cudaMallocAsync(&dk, kb, st) != cudaSuccess ||
+        cudaMallocAsync(&dv, kb, st) != cudaSuccess || cudaMallocAsync(&dout, qb, st) != cudaSuccess ||
+        cudaMallocAsync(&ws, wsb, st) != cudaSuccess) {
+        cudaGetLastError();
+        rc = SAGE2_ENOMEM;
+    }
+    if (rc == SAGE2_OK) {
+        if (cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            rc = SAGE2_ECUDA;
+    }
+    if (rc == SAGE2_OK) rc = sage2_attn_ws(dq, dk, dv, dout, B, H_q, H_kv, N, d, causal, ws, wsb, stream);
+    if (rc == SAGE2_OK && cudaMemcpyAsync(out_host, dout, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = SAGE2_ECUDA;
+    for (void* p : {dq, dk, dv, dout, ws})
+        if (p) cudaFreeAsync(p, st);
+    return rc;
+}
+
+int sage2_probe_accumulator(const uint32_t* d_bits, const uint8_t* prod_vals, int n, uint32_t* c_zero,
+                            uint32_t* c_prod) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (n < 0 || (n > 0 && (!d_bits || !prod_vals || !c_zero || !c_prod))) return SAGE2_EINVAL;
+    return run_probe_accumulator(d_bits, prod_vals, n, c_zero, c_prod);
+}
+
+int sage2_bench_mma(int kind, int iters, double* ops_per_s) {
+    int rc = check_device();
+    if (rc) return rc;
+    if ((kind != 0 && kind != 1) || iters < 1 || !ops_per_s) return SAGE2_EINVAL;
+    return run_bench_mma(kind, iters, ops_per_s);
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""Thin ctypes binding over libsage2.so (include/sage2.h).  Argument marshalling only: every step
+of the SageAttention2 forward runs in the library's CUDA kernels.  PyTorch is used only for device
+memory and streams.  There is no CPU fallback: if libsage2.so is missing or the GPU is not sm_100,
+these functions raise.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsage2.so")
+
+F_CAUSAL = 1
+F_INT8 = 2
+WS_NREGIONS = 12
+REGIONS = ("ksum", "vmax", "kbar", "dv", "qhat", "dq", "qbar", "khat", "dk", "vhat", "ds", "end")
+
+_lib = None
+
+
+class Sage2Error(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libsage2.so (built in-tree by paper_2411_10958_b200.build).  Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise Sage2Error(f"{LIB_PATH} is missing: run `python -m paper_2411_10958_b200.build` "
+                             "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        L.sage2_version.restype = I
+        L.sage2_strerror.restype = ctypes.c_char_p
+        L.sage2_strerror.argtypes = [I]
+        L.sage2_workspace_bytes.restype = S
+        L.sage2_workspace_bytes.argtypes = [I] * 6
+        L.sage2_attn.argtypes = [P, P, P, P] + [I] * 6 + [P]
+        L.sage2_attn_ws.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
+        L.sage2_attn_ex.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
+        L.sage2_workspace_layout.argtypes = [I] * 5 + [ctypes.POINTER(S)]
+        L.sage2_prepare.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
+        L.sage2_attention.argtypes = [P] + [I] * 6 + [P, S, P]
+        L.sage2_debug_qk_int32.argtypes = [P, P] + [I] * 6 + [P, S, P]
+        L.sage2_probe_accumulator.argtypes = [P, P, I, P, P]
+        L.sage2_bench_mma.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
+        L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
+        for n in ("sage2_attn", "sage2_attn_ws", "sage2_attn_ex", "sage2_workspace_layout", "sage2_prepare",
+                  "sage2_attention", "sage2_debug_qk_int32", "sage2_probe_accumulator", "sage2_bench_mma",
+                  "sage2_attn_host"):
+            getattr(L, n).restype = I
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise Sage2Error(f"libsage2 error {rc}: {lib().sage2_strerror(rc).decode()}")
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _shape(q, k):
+    B, Hq, N, d = q.shape
+    Hkv = k.shape[1]
+    return B, Hq, Hkv, N, d
+
+
+def _check_inputs(q, k, v):
+    for t in (q, k, v):
+        if t.dtype != torch.float16 or not t.is_cuda or not t.is_contiguous() or t.dim() != 4:
+            raise ValueError("q, k, v must be contiguous fp16 CUDA tensors [B, H, N, d]")
+    if k.shape != v.shape or q.shape[0] != k.shape[0] or q.shape[2:] != k.shape[2:]:
+        raise ValueError("shape mismatch: q [B,Hq,N,d], k/v [B,Hkv,N,d]")
+
+
+def flags(causal=False, int8=False):
+    return (F_CAUSAL if causal else 0) | (F_INT8 if int8 else 0)
+
+
+def workspace_bytes(B, Hq, Hkv, N, d):
+    return int(lib().sage2_workspace_bytes(B, Hq, Hkv, N, d, 0))
+
+
+def layout(B, Hq, Hkv, N, d):
+    offs = (ctypes.c_size_t * WS_NREGIONS)()
+    _check(lib().sage2_workspace_layout(B, Hq, Hkv, N, d, offs))
+    return dict(zip(REGIONS, [int(o) for o in offs]))
+
+
+def alloc_workspace(B, Hq, Hkv, N, d, device="cuda"):
+    return torch.empty(workspace_bytes(B, Hq, Hkv, N, d), dtype=torch.uint8, device=device)
+
+
+def attn(q, k, v, causal=False, int8=False, out=None, workspace=None):
+    """SageAttn2 forward: q [B,Hq,N,d], k/v [B,Hkv,N,d] fp16 CUDA -> out [B,Hq,N,d] fp16."""
+    _check_inputs(q, k, v)
+    B, Hq, Hkv, N, d = _shape(q, k)
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None and not int8:
+        _check(lib().sage2_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
+                                int(causal), _stream()))
+        return out
+    if workspace is None:
+        workspace = alloc_workspace(B, Hq, Hkv, N, d, q.device)
+    _check(lib().sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
+                               flags(causal, int8), workspace.data_ptr(), workspace.numel(), _stream()))
+    return out
+
+
+def prepare(q, k, v, workspace, causal=False, int8=False):
+    """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`."""
+    _check_inputs(q, k, v)
+    B, Hq, Hkv, N, d = _shape(q, k)
+    _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8),
+                               workspace.data_ptr(), workspace.numel(), _stream()))
+
+
+def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False):
+    """The tcgen05 attention kernel only, on a prepared workspace."""
+    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8), workspace.data_ptr(),
+                                 workspace.numel(), _stream()))
+    return out
+
+
+def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False):
+    """Runs the attention kernel (non-causal) and returns the raw INT32 S = Q^ K^T read from TMEM,
+    [B*Hq, N_pad, N_pad]."""
+    Np = (N + 127) // 128 * 128
+    s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
+    _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), B, Hq, Hkv, N, d, flags(False, int8),
+                                      workspace.data_ptr(), workspace.numel(), _stream()))
+    return s
+
+
+def attn_host(q, k, v, out, causal=False):
+    """End-to-end C-ABI call on HOST buffers (pinned recommended): H2D copies, preprocessing,
+    attention and the D2H copy of out all happen inside sage2_attn_host on `stream`."""
+    for t in (q, k, v, out):
+        if t.is_cuda or t.dtype != torch.float16 or not t.is_contiguous():
+            raise ValueError("attn_host expects contiguous fp16 host tensors")
+    B, Hq, Hkv, N, d = _shape(q, k)
+    _check(lib().sage2_attn_host(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
+                                 int(causal), _stream()))
+    return out
+
+
+def probe_accumulator(d_bits, prod_vals):
+    """FP22 probe on tcgen05 kind::f8f6f4.  d_bits: uint32 numpy, prod_vals: uint8 (E4M3)."""
+    import numpy as np
+    d_bits = np.ascontiguousarray(d_bits, dtype=np.uint32)
+    prod_vals = np.ascontiguousarray(prod_vals, dtype=np.uint8)
+    n = d_bits.size
+    cz = np.zeros(n, np.uint32)
+    cp = np.zeros(n, np.uint32)
+    _check(lib().sage2_probe_accumulator(d_bits.ctypes.data, prod_vals.ctypes.data, n, cz.ctypes.data,
+                                         cp.ctypes.data))
+    return cz, cp
+
+
+def bench_mma(kind, iters=20000):
+    """Dense tcgen05 throughput, ops/s.  kind 0 = kind::i8, 1 = kind::f8f6f4 (E4M3)."""
+    r = ctypes.c_double()
+    _check(lib().sage2_bench_mma(int(kind), int(iters), ctypes.byref(r)))
+    return r.value
+
+
+def version():
+    return int(lib().sage2_version())

@@ -1,0 +1,48 @@
+"""The C-ABI library loads on a CPU-only box and exports every symbol include/sage2.h declares
+(no compute calls: those need a B200)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sage2.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sage2_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("sage2_attn", "sage2_attn_ws", "sage2_workspace_bytes", "sage2_prepare", "sage2_attention",
+              "sage2_debug_qk_int32", "sage2_strerror", "sage2_version", "sage2_attn_host"):
+        assert s in syms
+
+
+def test_library_builds_loads_and_exports_all_symbols():
+    from paper_2411_10958_b200 import build
+    path = build.build()
+    L = ctypes.CDLL(path)
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+    L.sage2_version.restype = ctypes.c_int
+    assert L.sage2_version() >= 1
+    L.sage2_strerror.restype = ctypes.c_char_p
+    assert b"sm_100" in L.sage2_strerror(-2)
+    L.sage2_workspace_bytes.restype = ctypes.c_size_t
+    assert L.sage2_workspace_bytes(1, 1, 1, 256, 64, 0) > 0
+    assert L.sage2_workspace_bytes(1, 1, 1, 256, 96, 0) == 0          # d = 96 invalid
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        return
+    from paper_2411_10958_b200 import sage2
+    q = torch.zeros((1, 1, 128, 64), dtype=torch.float16)
+    try:
+        sage2.attn(q, q, q)
+    except (ValueError, sage2.Sage2Error):
+        return
+    raise AssertionError("attn on CPU tensors must raise (no CPU fallback)")
