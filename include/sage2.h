@@ -108,9 +108,11 @@ int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags
 
 /* Debug: runs the attention kernel non-causally and additionally writes the raw INT32 QK^T
  * accumulators read back from TMEM to s_int [B*H_q][N_pad][N_pad] (device, caller-owned,
- * 4*B*H_q*N_pad^2 bytes; intended for small N).  out receives the normal output. */
-int sage2_debug_qk_int32(void* out, int32_t* s_int, int B, int H_q, int H_kv, int N, int d, int flags,
-                         const void* workspace, size_t ws_bytes, void* stream);
+ * 4*B*H_q*N_pad^2 bytes; intended for small N) and, if p_hat is not NULL, the E4M3 codes of
+ * P^ = e4m3(448 P~) the kernel fed to the PV MMA, [B*H_q][N_pad][N_pad] bytes (rows of later KV
+ * tiles hold the codes computed with the running max at that tile).  out receives the output. */
+int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H_q, int H_kv, int N, int d,
+                         int flags, const void* workspace, size_t ws_bytes, void* stream);
 
 /* Probe (the experiment of P:284-285 repeated on tcgen05).  For each of n
  * fp32 bit patterns D[i] (host array) the accumulator of tcgen05.mma.kind::f8f6f4 (M=128, N=32,

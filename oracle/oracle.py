@@ -32,7 +32,7 @@ def build(force=False):
 class _Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "b_q", "kv_tile", "causal", "quant", "qk_max", "smooth_q", "smooth_k",
-        "pv_mode", "two_level", "smooth_v")]
+        "pv_mode", "two_level", "smooth_v", "p_fp32")] + [("amb_eta", ctypes.c_double)]
 
 
 @dataclass
@@ -48,11 +48,13 @@ class OracleConfig:
     pv_mode: int = 0          # 0 fp64 R, 1 fp32 R, 2 FP22-truncated R
     two_level: bool = True
     smooth_v: bool = False
+    p_fp32: bool = True       # P^ decision in the kernel's precision (C-21)
+    amb_eta: float = 2.0 ** -12
 
     def c(self):
         return _Cfg(self.b_q, self.kv_tile, int(self.causal), int(self.quant), self.qk_max,
                     int(self.smooth_q), int(self.smooth_k), self.pv_mode, int(self.two_level),
-                    int(self.smooth_v))
+                    int(self.smooth_v), int(self.p_fp32), float(self.amb_eta))
 
 
 def lib():
@@ -80,6 +82,8 @@ def lib():
             L.orc_delta_s.argtypes = [P, P, I, I, P]
             L.orc_s_int_block.argtypes = [P, P, I, I, P]
             L.orc_attn_block_q.argtypes = [P, P, P, P, P, P, P, P, I, I, I, ctypes.POINTER(_Cfg), P, P]
+            L.orc_attn_block_dbg.argtypes = [P, P, P, P, P, P, P, P, I, I, I, ctypes.POINTER(_Cfg), P, P,
+                                             P, P, P]
             L.orc_attn_exact_tiled.argtypes = [P, P, P, I, I, ctypes.POINTER(_Cfg), I, I, P]
             _lib = L
     return _lib
@@ -194,17 +198,27 @@ def s_int_block(qhat, khat):
     return out
 
 
-def attn_block(qb, ds, kv, N, i, cfg=OracleConfig()):
-    """Alg. 1 inner loop for Q block i. Returns (O[128,d] fp64, l[128])."""
+def attn_block(qb, ds, kv, N, i, cfg=OracleConfig(), debug=False):
+    """Alg. 1 inner loop for Q block i. Returns (O[128,d] fp64, l[128]) and, with debug=True,
+    a dict with the P^ codes [128, N_pad], ambiguity flags and per-row flip bounds."""
     d = qb["qhat"].shape[1]
+    Np = (N + 127) // 128 * 128
     O = np.zeros((128, d), np.float64)
     l = np.zeros(128, np.float64)
     ds = _c(ds, np.float64)
     c = cfg.c()
-    lib().orc_attn_block_q(_p(qb["qhat"]), _p(qb["dq"]), _p(ds), _p(kv["khat"]), _p(kv["dk"]),
-                           _p(kv["vhat"]), _p(kv["dv"]), _p(kv["vmean"]), N, d, i,
-                           ctypes.byref(c), _p(O), _p(l))
-    return O, l
+    if not debug:
+        lib().orc_attn_block_q(_p(qb["qhat"]), _p(qb["dq"]), _p(ds), _p(kv["khat"]), _p(kv["dk"]),
+                               _p(kv["vhat"]), _p(kv["dv"]), _p(kv["vmean"]), N, d, i,
+                               ctypes.byref(c), _p(O), _p(l))
+        return O, l
+    ph = np.zeros((128, Np), np.uint8)
+    amb = np.zeros((128, Np), np.uint8)
+    flip = np.zeros(128, np.float64)
+    lib().orc_attn_block_dbg(_p(qb["qhat"]), _p(qb["dq"]), _p(ds), _p(kv["khat"]), _p(kv["dk"]),
+                             _p(kv["vhat"]), _p(kv["dv"]), _p(kv["vmean"]), N, d, i,
+                             ctypes.byref(c), _p(O), _p(l), _p(ph), _p(amb), _p(flip))
+    return O, l, dict(phat=ph, amb=amb, flip=flip)
 
 
 def attn_exact_tiled(Q, K, V, cfg=OracleConfig(quant=False), row0=0, row1=None):
@@ -218,18 +232,19 @@ def attn_exact_tiled(Q, K, V, cfg=OracleConfig(quant=False), row0=0, row1=None):
     return O
 
 
-def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False):
+def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False, debug=False):
     """SageAttn2 forward on selected Q blocks.
 
     q: [B, Hq, N, d] fp16 numpy; k, v: [B, Hkv, N, d].  units: iterable of (b, h_q, i).
     Returns dict with 'O' [n_units, 128, d] fp64 (pre-rounding), 'O16' (fp16-rounded, fp64
-    array), and when keep=True the per-unit intermediates.
+    array), 'flip' [n_units, 128] (debug=True: per-row bound on the effect of ambiguous P^
+    decisions, C-21) and when keep=True the per-unit intermediates (incl. P^ codes).
     """
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
     grp = Hq // Hkv
     kv_cache = {}
-    outO, outO16, inter = [], [], []
+    outO, outO16, inter, flips = [], [], [], []
     for (b, h, i) in units:
         hk = h // grp
         if (b, hk) not in kv_cache:
@@ -238,12 +253,19 @@ def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False):
         r0, r1 = 128 * i, min(128 * i + 128, N)
         qb = q_block(q[b, h, r0:r1], cfg)
         ds = delta_s(qb["qbar"], kv["kprime"])
-        O, l = attn_block(qb, ds, kv, N, i, cfg)
+        if debug:
+            O, l, dbg = attn_block(qb, ds, kv, N, i, cfg, debug=True)
+            flips.append(dbg["flip"])
+        else:
+            O, l = attn_block(qb, ds, kv, N, i, cfg)
+            dbg = None
         outO.append(O)
         outO16.append(fp16_round(O))
         if keep:
-            inter.append(dict(qb=qb, ds=ds, l=l))
+            inter.append(dict(qb=qb, ds=ds, l=l, dbg=dbg))
     res = dict(O=np.stack(outO), O16=np.stack(outO16))
+    if debug:
+        res["flip"] = np.stack(flips)
     if keep:
         res["inter"] = inter
         res["kv"] = kv_cache

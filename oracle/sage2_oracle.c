@@ -47,6 +47,11 @@ typedef struct {
                        every 32-wide K step                            */
     int two_level;  /* 1: R fresh per tile then O = alpha O + R;  0: single level   */
     int smooth_v;   /* optional smooth V; NEXT#2                                    */
+    int p_fp32;     /* 1: the P^ code decision is taken in the kernel's precision (fp32 scores in
+                       base 2, P~*448 rounded to fp32 before the E4M3 cast) -- DESIGN.md C-21;
+                       0: everything in fp64 (the paper's formulas verbatim)                    */
+    double amb_eta; /* relative distance to an E4M3 rounding midpoint under which a P^ decision is
+                       reported "ambiguous" (the fp32 precision gap, C-21)             */
 } orc_cfg;
 
 /* ------------------------------------------------------------------------------------------ */
@@ -292,33 +297,66 @@ int orc_s_int_block(const int8_t* qhat, const int8_t* khat, int Np, int d, int64
 /* ------------------------------------------------------------------------------------------ */
 /* Algorithm 1 inner loop for one Q block i (rows 128 i .. 128 i + 127), quantized path.      */
 /* ------------------------------------------------------------------------------------------ */
+
+/* Distance (relative) from v > 0 to the nearest E4M3 rounding midpoint around its code, and the
+ * larger of the two neighbouring code gaps.  Used only for the ambiguity report. */
+static double e4m3_midpoint_gap(double v, const double* e4m3, double* ulp_out) {
+    uint8_t c = orc_e4m3_encode(v);
+    double x = e4m3[c], best = INFINITY, ulp = 0.0;
+    if (c > 0) {                                   /* lower neighbour (positive codes only) */
+        double lo = e4m3[c - 1], mid = 0.5 * (lo + x);
+        best = fabs(v - mid) / v;
+        ulp = x - lo;
+    }
+    if (c < 0x7e) {
+        double hi = e4m3[c + 1], mid = 0.5 * (x + hi);
+        double g = fabs(v - mid) / v;
+        if (g < best) best = g;
+        if (hi - x > ulp) ulp = hi - x;
+    }
+    *ulp_out = ulp;
+    return best;
+}
+
 /* Inputs: the block's qhat[128*d], dq[32], ds[N] (Delta S_i), the head's khat/dk/vhat/dv,
  * vmean (smooth_v).  Output: O[128*d] fp64 before fp16 rounding (rows >= N set to 0),
- * and, if l_out != NULL, the final row sums l (diagnostics). */
-int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,
-                     const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
-                     const float* vmean, int N, int d, int i, const orc_cfg* cfg,
-                     double* O, double* l_out) {
+ * and optionally: l_out[128] final row sums (in units of P~), phat_out[128*Np] the P^ codes,
+ * amb_out[128*Np] ambiguity flags, flip_out[128] = sum over ambiguous keys of
+ * gap(P^) * max_c |V^ dV| / (448 l): how far O could move if every ambiguous decision flipped. */
+int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
+                       const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
+                       const float* vmean, int N, int d, int i, const orc_cfg* cfg,
+                       double* O, double* l_out, uint8_t* phat_out, uint8_t* amb_out, double* flip_out) {
     const double inv_sqrt_d = 1.0 / sqrt((double)d);      /* P:77 scale 1/sqrt(d) (C-11) */
+    const double LOG2E = 1.4426950408889634;
+    const double LOG2_448 = log2(448.0);
     const int bkv = cfg->kv_tile;
     int Np = (N + 127) / 128 * 128;
-    /* decode tables once */
     double e4m3[256];
     for (int c = 0; c < 256; ++c) e4m3[c] = orc_e4m3_decode((uint8_t)c);
+    double* vmax_t = (double*)calloc((size_t)Np, sizeof(double));   /* max_c |V^ dV| per key */
+    for (int t = 0; t < N; ++t)
+        for (int c = 0; c < d; ++c) {
+            double a = fabs(e4m3[vhat[(size_t)t * d + c]]) * (double)dv[c];
+            if (a > vmax_t[t]) vmax_t[t] = a;
+        }
 
 #pragma omp parallel for schedule(dynamic, 4)
     for (int rr = 0; rr < 128; ++rr) {
         int r = 128 * i + rr;                       /* global query index */
         double* o = O + (size_t)rr * d;
         for (int c = 0; c < d; ++c) o[c] = 0.0;
-        if (r >= N) { if (l_out) l_out[rr] = 0.0; continue; }
+        if (phat_out) memset(phat_out + (size_t)rr * Np, 0, (size_t)Np);
+        if (amb_out) memset(amb_out + (size_t)rr * Np, 0, (size_t)Np);
+        if (r >= N) { if (l_out) l_out[rr] = 0.0; if (flip_out) flip_out[rr] = 0.0; continue; }
         double* R = (double*)malloc(sizeof(double) * d);
         double* S = (double*)malloc(sizeof(double) * bkv);
-        double m = -INFINITY, l = 0.0;
+        double m = -INFINITY, l = 0.0, flip = 0.0;
         int kend = cfg->causal ? r + 1 : N;          /* keys visible to this row (C-18) */
         for (int j0 = 0; j0 < kend; j0 += bkv) {     /* KV tiles in ascending order (C-9) */
             int j1 = j0 + bkv;
-            /* (a)+(b) S = (psi^-1(Q^ K^T) + Delta S) / sqrt(d); masked -> -inf */
+            /* (a)+(b) S = (psi^-1(Q^ K^T) + Delta S) / sqrt(d); masked -> -inf.
+             * p_fp32 (C-21): scores kept as fp32 values in base 2, S * log2(e). */
             double tmax = -INFINITY;
             for (int t = j0; t < j1; ++t) {
                 double s;
@@ -328,14 +366,16 @@ int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,
                     for (int c = 0; c < d; ++c)
                         si += (int64_t)qhat[(size_t)rr * d + c] * (int64_t)khat[(size_t)t * d + c];
                     s = ((double)si * (double)dq[orc_group_q(rr)] * (double)dk[orc_group_k(t)] + ds[t]) * inv_sqrt_d;
+                    if (cfg->p_fp32) s = (double)(float)(s * LOG2E);
                 }
                 S[t - j0] = s;
                 if (s > tmax) tmax = s;
             }
-            /* (c) online softmax */
+            /* (c) online softmax: m_ij = max(m_i,j-1, rowmax S_ij) exactly (C-10) */
             double m_new = (tmax > m) ? tmax : m;
-            double alpha = (m == -INFINITY) ? 0.0 : exp(m - m_new);
+            double alpha = (m == -INFINITY) ? 0.0 : (cfg->p_fp32 ? exp2(m - m_new) : exp(m - m_new));
             double rowsum = 0.0;
+            flip *= alpha;
             /* Level-1 accumulator.  two_level: R fresh per tile ("R_ij = P~_ij V_j").
              * single level (ablation): the running O itself is the MMA accumulator, rescaled
              * first (Eq. 1).  Precision per pv_mode: fp64, fp32, or FP22. */
@@ -351,10 +391,24 @@ int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,
                 }
             }
             for (int t = j0; t < j1; ++t) {
-                double p = (S[t - j0] == -INFINITY) ? 0.0 : exp(S[t - j0] - m_new);   /* P~ */
-                rowsum += p;                                                     /* C-13 */
-                /* (d) P^ = E4M3(448 * P~)  (P:256, P:277) */
-                double ph = e4m3[orc_e4m3_encode(448.0 * p)];
+                /* P~ = exp(S - m) ; the E4M3 operand is 448 * P~ */
+                double p448;
+                if (S[t - j0] == -INFINITY) p448 = 0.0;
+                else if (cfg->p_fp32) p448 = (double)(float)exp2(S[t - j0] - m_new + LOG2_448);
+                else p448 = 448.0 * exp(S[t - j0] - m_new);
+                rowsum += p448 / 448.0;                                          /* C-13 */
+                /* (d) P^ = E4M3(448 * P~) */
+                uint8_t code = orc_e4m3_encode(p448);
+                double ph = e4m3[code];
+                if (phat_out && t < Np) phat_out[(size_t)rr * Np + t] = code;
+                if (p448 > 0.0 && (amb_out || flip_out)) {
+                    double ulp;
+                    double gap = e4m3_midpoint_gap(p448, e4m3, &ulp);
+                    if (gap <= cfg->amb_eta) {
+                        if (amb_out && t < Np) amb_out[(size_t)rr * Np + t] = 1;
+                        flip += ulp * vmax_t[t];      /* divided by 448 l at the end */
+                    }
+                }
                 if (ph != 0.0) {
                     /* (e) acc += P^ V^  ("Matmul((P~*448).to(FP8.e4m3), V_j)") */
                     for (int c = 0; c < d; ++c) {
@@ -377,10 +431,19 @@ int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,
         /* O-9: O_i = diag(l)^-1 O / 448 * delta_V (+ V_m if smooth V) */
         for (int c = 0; c < d; ++c) o[c] = o[c] / l / 448.0 * (double)dv[c] + (double)vmean[c];
         if (l_out) l_out[rr] = l;
+        if (flip_out) flip_out[rr] = flip / (448.0 * l);
         free(R);
         free(S);
     }
+    free(vmax_t);
     return 0;
+}
+
+int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,
+                     const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
+                     const float* vmean, int N, int d, int i, const orc_cfg* cfg,
+                     double* O, double* l_out) {
+    return orc_attn_block_dbg(qhat, dq, ds, khat, dk, vhat, dv, vmean, N, d, i, cfg, O, l_out, NULL, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------------------------------ */

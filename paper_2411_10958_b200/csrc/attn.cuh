@@ -35,6 +35,7 @@ struct AttnParams {
     const float* ds;        // [B*Hq][nT][N_pad]  Delta S * log2(e)/sqrt(d)
     __half* out;            // [B][Hq][N][D]
     int32_t* s_dump;        // debug: [B*Hq][N_pad][N_pad] raw S_int (DUMP builds only)
+    uint8_t* p_dump;        // debug: [B*Hq][N_pad][N_pad] P^ codes (DUMP builds only; may be null)
     int Hq, Hkv, N, nT;
     float qk_scale_log2;    // log2(e)/sqrt(d)
 };
@@ -221,6 +222,9 @@ __global__ void __launch_bounds__(192, 1) k_attn(const AttnParams p) {
                     w[q] = lo | (hi << 16);
                 }
                 *reinterpret_cast<uint4*>(sP + swz_off<128>(row, c0)) = make_uint4(w[0], w[1], w[2], w[3]);
+                if (DUMP && p.p_dump)
+                    *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * (nT * 128) + grow) * (size_t)(nT * 128) +
+                                              j * 128 + c0) = make_uint4(w[0], w[1], w[2], w[3]);
             }
             fence_proxy_async_smem();
             mbar_arrive(bar_p_full);

@@ -120,7 +120,7 @@ int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
 }
 
-int launch_attention(void* out, int32_t* s_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
+int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
                      const Layout& L, cudaStream_t st) {
     AttnParams p;
     p.qhat = reinterpret_cast<const int8_t*>(ws + L.off[R_QHAT]);
@@ -132,6 +132,7 @@ int launch_attention(void* out, int32_t* s_dump, int B, int Hq, int Hkv, int N, 
     p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
     p.out = reinterpret_cast<__half*>(out);
     p.s_dump = s_dump;
+    p.p_dump = p_dump;
     p.Hq = Hq;
     p.Hkv = Hkv;
     p.N = N;
@@ -206,18 +207,18 @@ int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags
     if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out)) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
-    return launch_attention(out, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
+    return launch_attention(out, nullptr, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
                             reinterpret_cast<cudaStream_t>(stream));
 }
 
-int sage2_debug_qk_int32(void* out, int32_t* s_int, int B, int H_q, int H_kv, int N, int d, int flags,
-                         const void* workspace, size_t ws_bytes, void* stream) {
+int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H_q, int H_kv, int N, int d,
+                         int flags, const void* workspace, size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
-    return launch_attention(out, s_int, B, H_q, H_kv, N, d, flags & ~SAGE2_F_CAUSAL,
+    return launch_attention(out, s_int, p_hat, B, H_q, H_kv, N, d, flags & ~SAGE2_F_CAUSAL,
                             reinterpret_cast<const uint8_t*>(workspace), L, reinterpret_cast<cudaStream_t>(stream));
 }
 

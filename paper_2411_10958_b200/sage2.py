@@ -43,7 +43,7 @@ def lib():
         L.sage2_workspace_layout.argtypes = [I] * 5 + [ctypes.POINTER(S)]
         L.sage2_prepare.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
         L.sage2_attention.argtypes = [P] + [I] * 6 + [P, S, P]
-        L.sage2_debug_qk_int32.argtypes = [P, P] + [I] * 6 + [P, S, P]
+        L.sage2_debug_qk_int32.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
         L.sage2_probe_accumulator.argtypes = [P, P, I, P, P]
         L.sage2_bench_mma.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
         L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
@@ -128,14 +128,16 @@ def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False):
     return out
 
 
-def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False):
+def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False):
     """Runs the attention kernel (non-causal) and returns the raw INT32 S = Q^ K^T read from TMEM,
-    [B*Hq, N_pad, N_pad]."""
+    [B*Hq, N_pad, N_pad] (and, with_p=True, also the P^ E4M3 codes the kernel produced)."""
     Np = (N + 127) // 128 * 128
     s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
-    _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), B, Hq, Hkv, N, d, flags(False, int8),
-                                      workspace.data_ptr(), workspace.numel(), _stream()))
-    return s
+    ph = torch.zeros((B * Hq, Np, Np), dtype=torch.uint8, device=out.device) if with_p else None
+    _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
+                                      N, d, flags(False, int8), workspace.data_ptr(), workspace.numel(),
+                                      _stream()))
+    return (s, ph) if with_p else s
 
 
 def attn_host(q, k, v, out, causal=False):

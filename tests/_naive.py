@@ -62,8 +62,11 @@ def _quant_groups(X, groups, qmax, n_rows):
     return codes, deltas
 
 
-def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7):
-    """Q, K, V: [N, d] float16 numpy (one head).  Returns O [N, d] fp64 before fp16 rounding."""
+def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True):
+    """Q, K, V: [N, d] float16 numpy (one head).  Returns O [N, d] fp64 before fp16 rounding.
+
+    p_fp32: scores held as fp32 in base 2 (S log2 e) and 448 P~ rounded to fp32 before the
+    E4M3 cast -- the kernel's precision for that decision (C-21); else fp64 with exp."""
     N, d = Q.shape
     n_pad = -(-N // 128) * 128
     Kf = K.astype(np.float32)
@@ -103,14 +106,22 @@ def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7):
                 for t in keys:
                     s_int = int(sum(int(qhat[rr, c]) * int(khat[t, c]) for c in range(d)))
                     S[t] = (s_int * float(dq_of[rr]) * float(dk_of[t]) + dS[t]) / math.sqrt(d)
+                    if p_fp32:
+                        S[t] = float(np.float32(S[t] * math.log2(math.e)))
                 m_new = max([m] + list(S.values()))
-                alpha = 0.0 if m == -math.inf else math.exp(m - m_new)
+                if p_fp32:
+                    alpha = 0.0 if m == -math.inf else 2.0 ** (m - m_new)
+                else:
+                    alpha = 0.0 if m == -math.inf else math.exp(m - m_new)
                 R = np.zeros(d)
                 rs = 0.0
                 for t in keys:
-                    p = math.exp(S[t] - m_new)
-                    rs += p
-                    R += _e4m3(448.0 * p) * vhat[t]
+                    if p_fp32:
+                        p448 = float(np.float32(2.0 ** (S[t] - m_new + math.log2(448.0))))
+                    else:
+                        p448 = 448.0 * math.exp(S[t] - m_new)
+                    rs += p448 / 448.0
+                    R += _e4m3(p448) * vhat[t]
                 l = alpha * l + rs
                 o = alpha * o + R
                 m = m_new

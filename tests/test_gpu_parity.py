@@ -4,8 +4,13 @@ Bar (DESIGN.md "Parity"):
   * codes, scales, means (Q^, K^, V^, delta_Q, delta_K, delta_V, q_bar, k_bar): bit-exact;
   * S_int = Q^ K^T read back from TMEM: bit-exact;
   * Delta S: |gpu - oracle| <= 2e-6 * sum_c |q_bar_c| |K'_tc|   (fp32 FMA chain vs fp64 sum);
-  * O: elementwise |O_gpu - O_oracle16| <= max(2e-3, 1 fp16 ulp(|O_oracle|)) and CosSim >= 0.9999
-    (north_star tolerance; O_oracle16 = oracle output rounded to fp16).
+  * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA: identical to the oracle's except where
+    the oracle marks the decision ambiguous (448 P~ within 2^-12 relative of an E4M3 rounding
+    midpoint: the fp32 precision gap between two correct implementations, C-21), and
+    there at most one code apart;
+  * O: elementwise |O_gpu - O_oracle16| <= max(2e-3, 1 fp16 ulp(|O_oracle|)) + F_r, where F_r is
+    the oracle's bound on what flipping row r's ambiguous P^ decisions can move O (0 for almost
+    every row), and CosSim >= 0.9999 (north_star tolerance; O_oracle16 = oracle O rounded to fp16).
 """
 import math
 
@@ -98,19 +103,52 @@ def test_s_int_bit_exact(N, d):
             assert np.array_equal(s[hq, 128 * i:128 * i + 128].astype(np.int64), ref)
 
 
+@pytest.mark.parametrize("N,d,kind", [(256, 64, "iid"), (384, 128, "structured"), (1000, 128, "structured")])
+def test_phat_codes(N, d, kind):
+    B, Hq, Hkv = 1, 2, 1
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=7)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws)
+    out = torch.empty_like(qg)
+    _, ph = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, with_p=True)
+    torch.cuda.synchronize()
+    ph = ph.cpu().numpy()
+    units = [(0, h, i) for h in range(Hq) for i in range((N + 127) // 128)]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(), keep=True, debug=True)
+    n_amb = n_diff = 0
+    for u, (b, h, i) in enumerate(units):
+        dbg = res["inter"][u]["dbg"]
+        r1 = min(N, 128 * i + 128) - 128 * i
+        g = ph[h, 128 * i:128 * i + r1, :N]
+        o = dbg["phat"][:r1, :N]
+        amb = dbg["amb"][:r1, :N].astype(bool)
+        diff = g != o
+        assert not np.any(diff & ~amb), f"unit {(b, h, i)}: P^ differs on {int((diff & ~amb).sum())} unambiguous keys"
+        assert np.all(np.abs(g[diff].astype(int) - o[diff].astype(int)) <= 1)
+        n_amb += int(amb.sum())
+        n_diff += int(diff.sum())
+    print(f"P^ codes: {n_diff} differ, all within the {n_amb} ambiguous decisions")
+
+
 def _compare_out(o_gpu, res, units, N):
-    errs, coss = [], []
+    """Returns (max abs err, min cos, rows that needed their flip allowance)."""
+    errs, coss, flipped = [], [], 0
     for u, (b, h, i) in enumerate(units):
         r0, r1 = 128 * i, min(N, 128 * i + 128)
         ref16 = res["O16"][u, : r1 - r0]
         got = o_gpu[b, h, r0:r1].astype(np.float64)
-        tol = np.maximum(2e-3, fp16_ulp(ref16))
+        base = np.maximum(2e-3, fp16_ulp(ref16))
+        flip = res["flip"][u, : r1 - r0, None] * (1 + 1e-6) + 1e-7
         err = np.abs(got - ref16)
-        assert np.all(err <= tol), f"unit {(b, h, i)}: max err {err.max():.3e} at {np.unravel_index(err.argmax(), err.shape)}"
+        ok = err <= base + flip
+        assert np.all(ok), (f"unit {(b, h, i)}: max err {err.max():.3e} at "
+                            f"{np.unravel_index(err.argmax(), err.shape)}, flip bound there "
+                            f"{res['flip'][u, np.unravel_index(err.argmax(), err.shape)[0]]:.3e}")
+        flipped += int(np.any(err > base, axis=1).sum())
         errs.append(err.max())
         coss.append(orc.cos_sim(res["O"][u, : r1 - r0], got))
     assert min(coss) >= 0.9999, coss
-    return max(errs), min(coss)
+    return max(errs), min(coss), flipped
 
 
 OUT_CASES = [
@@ -132,8 +170,10 @@ def test_output_parity(B, Hq, Hkv, N, d, causal, kind):
     out = sage2.attn(qg, kg, vg, causal=causal)
     torch.cuda.synchronize()
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
-    _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal),
+                                   debug=True)
+    err, cos, flipped = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    print(f"max|err|={err:.3e} min cos={cos:.8f} rows using flip allowance={flipped}")
 
 
 @pytest.mark.parametrize("causal", [False, True])
@@ -144,7 +184,7 @@ def test_int8_variant_parity(causal):
     torch.cuda.synchronize()
     units = [(0, h, i) for h in range(Hq) for i in range(3)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False))
+                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 

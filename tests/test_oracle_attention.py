@@ -93,17 +93,18 @@ def _oracle_head(orc, Q, K, V, cfg):
     return O
 
 
+@pytest.mark.parametrize("p_fp32", [True, False])
 @pytest.mark.parametrize("N,kv_tile,causal,kind", [
     (16, 128, False, "iid"), (16, 4, True, "iid"), (13, 4, False, "outlier"),
     (9, 2, True, "outlier")])
-def test_quantized_path_vs_naive(orc, N, kv_tile, causal, kind):
+def test_quantized_path_vs_naive(orc, N, kv_tile, causal, kind, p_fp32):
     d = 64
     if kind == "iid":
         Q, K, V = rnd((N, d), 20), rnd((N, d), 21), rnd((N, d), 22)
     else:
         Q, K, V = rnd((N, d), 23, 1, 4), rnd((N, d), 24, 1, -3), rnd((N, d), 25, 2, 8)
-    cfg = OracleConfig(kv_tile=kv_tile, causal=causal)
-    ref = sage2_naive(Q, K, V, causal=causal, kv_tile=kv_tile)
+    cfg = OracleConfig(kv_tile=kv_tile, causal=causal, p_fp32=p_fp32)
+    ref = sage2_naive(Q, K, V, causal=causal, kv_tile=kv_tile, p_fp32=p_fp32)
     got = _oracle_head(orc, Q, K, V, cfg)
     assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
 
