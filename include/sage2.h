@@ -52,6 +52,7 @@ extern "C" {
 #define SAGE2_F_CAUSAL 1   /* key <= query mask                                                  */
 #define SAGE2_F_INT8 2     /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing,  */
                            /* P:70, P:476 (Table 3)                                    */
+#define SAGE2_F_KERNEL_V0 4 /* use the simple one-Q-tile-per-CTA attention kernel (A/B checks)  */
 
 /* Library version (monotone integer). */
 int sage2_version(void);
@@ -127,6 +128,12 @@ int sage2_probe_accumulator(const uint32_t* d_bits, const uint8_t* prod_vals, in
  * 1 = f8f6f4 E4M3 M128 N256 K32) on every SM and returns the measured dense ops/s in *ops_per_s.
  * Synchronous. */
 int sage2_bench_mma(int kind, int iters, double* ops_per_s);
+
+/* Unit microbenchmarks (per-SM rates per SM clock; synchronous):
+ *   0 tcgen05.ld 32x32b bytes/clk, 1 tcgen05.st bytes/clk, 2 MUFU ex2 results/clk,
+ *   3 I2F results/clk, 4 FFMA2 lanes/clk, 5 legacy mma.sync m16n8k64 s4 ops/clk (the paper's Ada
+ *   INT4 instruction, emulated on sm_100a), 6 legacy mma.sync m16n8k32 s8 ops/clk. */
+int sage2_microbench(int which, int iters, double* per_clk_per_sm);
 
 #ifdef __cplusplus
 }

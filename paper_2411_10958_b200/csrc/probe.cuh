@@ -161,3 +161,143 @@ inline int run_bench_mma(int kind, int iters, double* ops_per_s) {
 }
 
 }  // namespace sage2
+
+namespace sage2 {
+
+// ---------------------------------------------------------------------------------------------
+// Unit microbenchmarks: per-SM throughputs that bound the softmax side of the kernel.
+//   which 0: tcgen05.ld 32x32b.x32  (bytes / clk / SM), 8 warps, 4 loads in flight per wait
+//   which 1: tcgen05.st 32x32b.x32  (bytes / clk / SM)
+//   which 2: MUFU ex2.approx.f32    (results / clk / SM)
+//   which 3: I2FP cvt.rn.f32.s32    (results / clk / SM)
+//   which 4: FFMA2 fma.rn.f32x2     (fp32 lanes / clk / SM)
+//   which 5: legacy mma.sync m16n8k64 s4.s4.s32   (ops / clk / SM)  -- the paper's Ada INT4 MMA
+//   which 6: legacy mma.sync m16n8k32 s8.s8.s32   (ops / clk / SM)
+// ---------------------------------------------------------------------------------------------
+template <int WHICH>
+__global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long* cyc, float* sink) {
+    __shared__ uint32_t tptr;
+    const int warp = threadIdx.x / 32;
+    if (WHICH <= 1) {
+        if (warp == 0) tmem_alloc<512>(smem_u32(&tptr));
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
+    const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t col0 = (warp >> 2) * 256;
+    uint32_t acc = threadIdx.x;
+    float f[8];
+    for (int i = 0; i < 8; ++i) f[i] = 0.001f * (threadIdx.x + i);
+    int ia[8];
+    for (int i = 0; i < 8; ++i) ia[i] = threadIdx.x * 3 + i;
+    unsigned long long x2[4];
+    for (int i = 0; i < 4; ++i) x2[i] = 0x3f8000003f800000ull + i;
+    uint32_t a4[4] = {threadIdx.x, 2u, 3u, 4u}, b2[2] = {5u, threadIdx.x}, c4[4] = {0, 0, 0, 0};
+    __syncthreads();
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        if (WHICH == 0) {
+            uint32_t r0[32], r1[32], r2[32], r3[32];
+            tmem_ld32(tptr + lane_off + col0 + 0, r0);
+            tmem_ld32(tptr + lane_off + col0 + 32, r1);
+            tmem_ld32(tptr + lane_off + col0 + 64, r2);
+            tmem_ld32(tptr + lane_off + col0 + 96, r3);
+            tmem_wait_ld();
+            reg_dep32(r0); reg_dep32(r1); reg_dep32(r2); reg_dep32(r3);
+            acc ^= r0[3] ^ r1[7] ^ r2[11] ^ r3[29];
+        } else if (WHICH == 1) {
+            uint32_t r0[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) r0[k] = acc + k;
+            tmem_st32(tptr + lane_off + col0 + 0, r0);
+            tmem_st32(tptr + lane_off + col0 + 32, r0);
+            tmem_st32(tptr + lane_off + col0 + 64, r0);
+            tmem_st32(tptr + lane_off + col0 + 96, r0);
+            tmem_wait_st();
+            acc += 1;
+        } else if (WHICH == 2) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = ex2_approx(f[i]);
+        } else if (WHICH == 3) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                f[i] += (float)ia[i];
+                ia[i] += 1;
+            }
+        } else if (WHICH == 4) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(x2[i]));
+        } else if (WHICH == 5) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                asm volatile(
+                    "mma.sync.aligned.m16n8k64.row.col.s32.s4.s4.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                    "{%0,%1,%2,%3};"
+                    : "+r"(c4[0]), "+r"(c4[1]), "+r"(c4[2]), "+r"(c4[3])
+                    : "r"(a4[0]), "r"(a4[1]), "r"(a4[2]), "r"(a4[3]), "r"(b2[0]), "r"(b2[1]));
+        } else if (WHICH == 6) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                asm volatile(
+                    "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                    "{%0,%1,%2,%3};"
+                    : "+r"(c4[0]), "+r"(c4[1]), "+r"(c4[2]), "+r"(c4[3])
+                    : "r"(a4[0]), "r"(a4[1]), "r"(a4[2]), "r"(a4[3]), "r"(b2[0]), "r"(b2[1]));
+        }
+    }
+    const long long t1 = clock64();
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = (unsigned long long)(t1 - t0);
+    float s = (float)acc + (float)(c4[0] ^ c4[1] ^ c4[2] ^ c4[3]);
+    for (int i = 0; i < 8; ++i) s += f[i] + (float)ia[i];
+    for (int i = 0; i < 4; ++i) s += (float)(x2[i] & 0xff);
+    if (s == 1234.5f) sink[threadIdx.x] = s;
+    if (WHICH <= 1) {
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) {
+            tc_fence_after();
+            tmem_dealloc<512>(tptr);
+        }
+    }
+}
+
+inline int run_micro(int which, int iters, double* per_clk_per_sm) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    unsigned long long* cyc = nullptr;
+    float* sink = nullptr;
+    if (cudaMalloc(&cyc, 8) != cudaSuccess || cudaMalloc(&sink, 1024) != cudaSuccess) return -4;
+    void (*kern)(int, unsigned long long*, float*) = nullptr;
+    switch (which) {
+        case 0: kern = k_micro<0>; break;
+        case 1: kern = k_micro<1>; break;
+        case 2: kern = k_micro<2>; break;
+        case 3: kern = k_micro<3>; break;
+        case 4: kern = k_micro<4>; break;
+        case 5: kern = k_micro<5>; break;
+        case 6: kern = k_micro<6>; break;
+        default: return -1;
+    }
+    kern<<<sms, 256>>>(16, cyc, sink);
+    kern<<<sms, 256>>>(iters, cyc, sink);
+    unsigned long long c = 0;
+    if (cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -4;
+    cudaFree(cyc);
+    cudaFree(sink);
+    const double per_iter_per_sm =
+        which == 0 ? 8.0 * 32 * 128 * 4            // bytes: 8 warps x 32 lanes x 128 cols x 4 B
+      : which == 1 ? 8.0 * 32 * 128 * 4
+      : which == 2 ? 256.0 * 8
+      : which == 3 ? 256.0 * 8
+      : which == 4 ? 256.0 * 8                      // 4 FFMA2 x 2 lanes
+      : which == 5 ? 8.0 * 4 * 2 * 16 * 8 * 64      // 8 warps x 4 mma x ops
+                   : 8.0 * 4 * 2 * 16 * 8 * 32;
+    *per_clk_per_sm = per_iter_per_sm * iters / (double)c;
+    return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+}  // namespace sage2

@@ -10,6 +10,7 @@
 
 #include "../../include/sage2.h"
 #include "attn.cuh"
+#include "attn2.cuh"
 #include "prep.cuh"
 #include "probe.cuh"
 
@@ -105,6 +106,21 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
 }
 
 template <int D, bool CAUSAL, bool DUMP>
+int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn2Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn2<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return SAGE2_ECUDA;
+        configured = true;
+    }
+    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+}
+
+template <int D, bool CAUSAL, bool DUMP>
 int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = AttnSmem<D>;
     // D=64 needs less shared memory; request enough to keep one CTA per SM (TMEM: 512 columns).
@@ -139,12 +155,20 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.nT = (N + 127) / 128;
     p.qk_scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
     const bool causal = (flags & SAGE2_F_CAUSAL) != 0;
-    if (s_dump) {
-        if (d == 64) return launch_attn_t<64, false, true>(p, B, st);
-        return launch_attn_t<128, false, true>(p, B, st);
+    if (flags & SAGE2_F_KERNEL_V0) {   // the simple one-tile kernel (kept for A/B checks)
+        if (s_dump) {
+            if (d == 64) return launch_attn_t<64, false, true>(p, B, st);
+            return launch_attn_t<128, false, true>(p, B, st);
+        }
+        if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
+        return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
     }
-    if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
-    return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
+    if (s_dump) {
+        if (d == 64) return launch_attn2_t<64, false, true>(p, B, st);
+        return launch_attn2_t<128, false, true>(p, B, st);
+    }
+    if (d == 64) return causal ? launch_attn2_t<64, true, false>(p, B, st) : launch_attn2_t<64, false, false>(p, B, st);
+    return causal ? launch_attn2_t<128, true, false>(p, B, st) : launch_attn2_t<128, false, false>(p, B, st);
 }
 
 int validate(const void* q, const void* k, const void* v, const void* out, int B, int Hq, int Hkv, int N, int d) {
@@ -298,6 +322,13 @@ int sage2_bench_mma(int kind, int iters, double* ops_per_s) {
     if (rc) return rc;
     if ((kind != 0 && kind != 1) || iters < 1 || !ops_per_s) return SAGE2_EINVAL;
     return run_bench_mma(kind, iters, ops_per_s);
+}
+
+int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (which < 0 || which > 6 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
+    return run_micro(which, iters, per_clk_per_sm);
 }
 
 }  // extern "C"

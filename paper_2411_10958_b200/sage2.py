@@ -47,6 +47,8 @@ def lib():
         L.sage2_probe_accumulator.argtypes = [P, P, I, P, P]
         L.sage2_bench_mma.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
         L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
+        L.sage2_microbench.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
+        L.sage2_microbench.restype = I
         for n in ("sage2_attn", "sage2_attn_ws", "sage2_attn_ex", "sage2_workspace_layout", "sage2_prepare",
                   "sage2_attention", "sage2_debug_qk_int32", "sage2_probe_accumulator", "sage2_bench_mma",
                   "sage2_attn_host"):
@@ -169,6 +171,17 @@ def bench_mma(kind, iters=20000):
     """Dense tcgen05 throughput, ops/s.  kind 0 = kind::i8, 1 = kind::f8f6f4 (E4M3)."""
     r = ctypes.c_double()
     _check(lib().sage2_bench_mma(int(kind), int(iters), ctypes.byref(r)))
+    return r.value
+
+
+MICRO = {0: "tmem_ld_bytes_per_clk_sm", 1: "tmem_st_bytes_per_clk_sm", 2: "mufu_ex2_per_clk_sm",
+         3: "i2f_per_clk_sm", 4: "ffma2_lanes_per_clk_sm", 5: "mma_sync_s4_ops_per_clk_sm",
+         6: "mma_sync_s8_ops_per_clk_sm"}
+
+
+def microbench(which, iters=4096):
+    r = ctypes.c_double()
+    _check(lib().sage2_microbench(int(which), int(iters), ctypes.byref(r)))
     return r.value
 
 

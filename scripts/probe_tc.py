@@ -50,6 +50,11 @@ def main():
     res["n"] = int(d.size)
     res["mma_i8_ops_per_s"] = sage2.bench_mma(0, 20000)
     res["mma_f8f6f4_ops_per_s"] = sage2.bench_mma(1, 20000)
+    for w, name in sage2.MICRO.items():
+        try:
+            res[name] = sage2.microbench(w, 4096)
+        except Exception as e:
+            res[name] = repr(e)
     print(json.dumps(res, indent=1))
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump(res, open("gpurun_out/probe.json", "w"), indent=1)
