@@ -54,6 +54,9 @@ extern "C" {
                            /* P:70, P:476 (Table 3)                                    */
 #define SAGE2_F_KERNEL_V0 4 /* use the simple one-Q-tile-per-CTA attention kernel (A/B checks)  */
 
+/* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
+const char* sage2_last_cuda_error(void);
+
 /* Library version (monotone integer). */
 int sage2_version(void);
 

@@ -19,19 +19,26 @@ using namespace sage2;
 namespace {
 
 constexpr int kVersion = 1;
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+
+int cuda_rc() {   // map the launch status to a return code, remembering the CUDA error
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) g_last_cuda_error = e;
+    return e == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+}
 
 int check_device() {
     static int state = 0;   // 0 unknown, 1 ok, -1 unsupported
     static std::mutex mu;
     std::lock_guard<std::mutex> g(mu);
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return SAGE2_ECUDA;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_rc();
     static int cached_dev = -1;
     if (state == 0 || cached_dev != dev) {
         int major = 0, minor = 0;
         if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
-            return SAGE2_ECUDA;
+            return cuda_rc();
         state = (major == 10 && minor == 0) ? 1 : -1;
         cached_dev = dev;
     }
@@ -86,7 +93,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const int qk_max = (flags & SAGE2_F_INT8) ? 127 : 7;
     const int smooth_q = (flags & SAGE2_F_INT8) ? 0 : 1;   // SageAttn2-8b: no Q smoothing
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
-    if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return SAGE2_ECUDA;
+    if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return cuda_rc();
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
     const int rows_per_cta = 512;
@@ -102,7 +109,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                 reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
                                                 scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]));
-    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+    return cuda_rc();
 }
 
 template <int D, bool CAUSAL, bool DUMP>
@@ -113,11 +120,11 @@ int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
     if (!configured) {
         if (cudaFuncSetAttribute(k_attn2<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
-            return SAGE2_ECUDA;
+            return cuda_rc();
         configured = true;
     }
-    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
-    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
+    return cuda_rc();
 }
 
 template <int D, bool CAUSAL, bool DUMP>
@@ -129,11 +136,11 @@ int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
     if (!configured) {
         if (cudaFuncSetAttribute(k_attn<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
-            return SAGE2_ECUDA;
+            return cuda_rc();
         configured = true;
     }
     k_attn<D, CAUSAL, DUMP><<<dim3(p.nT, p.Hq, B), 192, smem, st>>>(p);
-    return cudaGetLastError() == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
+    return cuda_rc();
 }
 
 int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
@@ -183,6 +190,8 @@ int validate(const void* q, const void* k, const void* v, const void* out, int B
 extern "C" {
 
 int sage2_version(void) { return kVersion; }
+
+const char* sage2_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
 const char* sage2_strerror(int code) {
     switch (code) {
@@ -276,7 +285,7 @@ int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, in
         return SAGE2_ENOMEM;
     }
     rc = sage2_attn_ws(q, k, v, out, B, H_q, H_kv, N, d, causal, ws, bytes, stream);
-    if (cudaFreeAsync(ws, st) != cudaSuccess && rc == SAGE2_OK) rc = SAGE2_ECUDA;
+    if (cudaFreeAsync(ws, st) != cudaSuccess && rc == SAGE2_OK) rc = cuda_rc();
     return rc;
 }
 
@@ -299,11 +308,11 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
         if (cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
             cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
             cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess)
-            rc = SAGE2_ECUDA;
+            rc = cuda_rc();
     }
     if (rc == SAGE2_OK) rc = sage2_attn_ws(dq, dk, dv, dout, B, H_q, H_kv, N, d, causal, ws, wsb, stream);
     if (rc == SAGE2_OK && cudaMemcpyAsync(out_host, dout, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        rc = SAGE2_ECUDA;
+        rc = cuda_rc();
     for (void* p : {dq, dk, dv, dout, ws})
         if (p) cudaFreeAsync(p, st);
     return rc;
@@ -329,6 +338,23 @@ int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
     if (rc) return rc;
     if (which < 0 || which > 6 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
     return run_micro(which, iters, per_clk_per_sm);
+}
+
+int sage2_debug_kernel_attrs(int d, int causal, int* out6) {
+    cudaFuncAttributes a{};
+    const void* f = d == 64 ? (causal ? (const void*)k_attn2<64, true, false> : (const void*)k_attn2<64, false, false>)
+                            : (causal ? (const void*)k_attn2<128, true, false> : (const void*)k_attn2<128, false, false>);
+    out6[0] = (int)cudaFuncGetAttributes(&a, f);
+    out6[1] = a.numRegs;
+    out6[2] = a.maxThreadsPerBlock;
+    out6[3] = (int)a.sharedSizeBytes;
+    out6[4] = a.maxDynamicSharedSizeBytes;
+    int nb = -1;
+    const size_t smem = d == 64 ? Attn2Smem<64>::ALLOC : Attn2Smem<128>::ALLOC;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 384, smem);
+    out6[5] = nb;
+    return (int)cudaGetLastError();
 }
 
 }  // extern "C"

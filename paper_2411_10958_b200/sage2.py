@@ -35,6 +35,7 @@ def lib():
         L.sage2_version.restype = I
         L.sage2_strerror.restype = ctypes.c_char_p
         L.sage2_strerror.argtypes = [I]
+        L.sage2_last_cuda_error.restype = ctypes.c_char_p
         L.sage2_workspace_bytes.restype = S
         L.sage2_workspace_bytes.argtypes = [I] * 6
         L.sage2_attn.argtypes = [P, P, P, P] + [I] * 6 + [P]
@@ -59,7 +60,10 @@ def lib():
 
 def _check(rc):
     if rc != 0:
-        raise Sage2Error(f"libsage2 error {rc}: {lib().sage2_strerror(rc).decode()}")
+        msg = lib().sage2_strerror(rc).decode()
+        if rc == -4:
+            msg += ": " + lib().sage2_last_cuda_error().decode()
+        raise Sage2Error(f"libsage2 error {rc}: {msg}")
 
 
 def _stream():
