@@ -123,7 +123,7 @@ int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
             return cuda_rc();
         configured = true;
     }
-    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
+    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
     return cuda_rc();
 }
 
