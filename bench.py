@@ -124,13 +124,8 @@ def barrier(world):
 
 
 def max_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2411_10958_b200.shard import max_over_ranks as mx
+    return mx(x, world, device="cuda")
 
 
 # ------------------------------------------------------------------------------------------------
@@ -209,7 +204,8 @@ def run_ours(args, world, rank, local):
     B, Hq, Hkv, N, d, causal, kind = CONFIGS[name]
     dev = torch.device("cuda", local if world > 1 else 0)
     # this rank's (b, h_kv) units: batch index offset by rank (weak scaling, independent units)
-    units = [(rank * B + b, h) for b in range(B) for h in range(Hkv)]
+    from paper_2411_10958_b200.shard import rank_units
+    units = rank_units(rank, world, B, Hkv)
     q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=0, device=dev, units=units)
     grp = Hq // Hkv
     q = q.view(B, Hkv, grp, N, d).reshape(B, Hq, N, d).contiguous()

@@ -11,6 +11,7 @@
 #include "../../include/sage2.h"
 #include "attn.cuh"
 #include "attn2.cuh"
+#include "attn4.cuh"
 #include "prep.cuh"
 #include "probe.cuh"
 
@@ -127,6 +128,21 @@ int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+template <int D, bool CAUSAL, bool DUMP, bool NULLSM = false, bool NULLMMA = false, bool TIMING = false>
+int launch_attn4_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn4Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn4<D, CAUSAL, DUMP, NULLSM, NULLMMA, TIMING>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    k_attn4<D, CAUSAL, DUMP, NULLSM, NULLMMA, TIMING><<<dim3(p.nT, p.Hq, B), 384, smem, st>>>(p);
+    return cuda_rc();
+}
+
 template <int D, bool CAUSAL, bool DUMP>
 int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = AttnSmem<D>;
@@ -142,6 +158,8 @@ int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
     k_attn<D, CAUSAL, DUMP><<<dim3(p.nT, p.Hq, B), 192, smem, st>>>(p);
     return cuda_rc();
 }
+
+int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st);
 
 int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
                      const Layout& L, cudaStream_t st) {
@@ -170,12 +188,37 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
         return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
     }
+    if (flags & (SAGE2_F_KERNEL_V4 | SAGE2_F_DEBUG_TIMING | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_NULLSM))
+        return launch_attention_v4(p, B, d, causal, s_dump != nullptr, flags, st);
+    // default: v1 -- two Q tiles per CTA, correction warpgroup, O in TMEM (attn2.cuh)
     if (s_dump) {
         if (d == 64) return launch_attn2_t<64, false, true>(p, B, st);
         return launch_attn2_t<128, false, true>(p, B, st);
     }
     if (d == 64) return causal ? launch_attn2_t<64, true, false>(p, B, st) : launch_attn2_t<64, false, false>(p, B, st);
     return causal ? launch_attn2_t<128, true, false>(p, B, st) : launch_attn2_t<128, false, false>(p, B, st);
+}
+
+// v4: one Q tile per CTA, key columns split over two warpgroups, triple-buffered S/R (attn4.cuh)
+int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st) {
+    if (flags & SAGE2_F_DEBUG_TIMING) {   // clock64 stamps of CTA (0,0,0) into s_dump (uint64)
+        if (d == 64) return launch_attn4_t<64, false, false, false, false, true>(p, B, st);
+        return launch_attn4_t<128, false, false, false, false, true>(p, B, st);
+    }
+    if (flags & SAGE2_F_DEBUG_NULLMMA) {  // timing experiment: softmax side only (wrong output)
+        if (d == 64) return launch_attn4_t<64, false, false, false, true>(p, B, st);
+        return launch_attn4_t<128, false, false, false, true>(p, B, st);
+    }
+    if (flags & SAGE2_F_DEBUG_NULLSM) {   // timing experiment: MMA/TMA pipeline only (wrong output)
+        if (d == 64) return launch_attn4_t<64, false, false, true>(p, B, st);
+        return launch_attn4_t<128, false, false, true>(p, B, st);
+    }
+    if (dump) {
+        if (d == 64) return launch_attn4_t<64, false, true>(p, B, st);
+        return launch_attn4_t<128, false, true>(p, B, st);
+    }
+    if (d == 64) return causal ? launch_attn4_t<64, true, false>(p, B, st) : launch_attn4_t<64, false, false>(p, B, st);
+    return causal ? launch_attn4_t<128, true, false>(p, B, st) : launch_attn4_t<128, false, false>(p, B, st);
 }
 
 int validate(const void* q, const void* k, const void* v, const void* out, int B, int Hq, int Hkv, int N, int d) {
@@ -342,15 +385,15 @@ int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
 
 int sage2_debug_kernel_attrs(int d, int causal, int* out6) {
     cudaFuncAttributes a{};
-    const void* f = d == 64 ? (causal ? (const void*)k_attn2<64, true, false> : (const void*)k_attn2<64, false, false>)
-                            : (causal ? (const void*)k_attn2<128, true, false> : (const void*)k_attn2<128, false, false>);
+    const void* f = d == 64 ? (causal ? (const void*)k_attn4<64, true, false> : (const void*)k_attn4<64, false, false>)
+                            : (causal ? (const void*)k_attn4<128, true, false> : (const void*)k_attn4<128, false, false>);
     out6[0] = (int)cudaFuncGetAttributes(&a, f);
     out6[1] = a.numRegs;
     out6[2] = a.maxThreadsPerBlock;
     out6[3] = (int)a.sharedSizeBytes;
     out6[4] = a.maxDynamicSharedSizeBytes;
     int nb = -1;
-    const size_t smem = d == 64 ? Attn2Smem<64>::ALLOC : Attn2Smem<128>::ALLOC;
+    const size_t smem = d == 64 ? Attn4Smem<64>::ALLOC : Attn4Smem<128>::ALLOC;
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 384, smem);
     out6[5] = nb;

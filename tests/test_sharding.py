@@ -1,0 +1,54 @@
+"""Multi-process (gloo, world_size 2, CPU) checks of the sharding host logic used by bench.py:
+units are disjoint and cover the global batch, inputs regenerated per unit are bit-identical to
+the unsharded generation, and the timing reduction is a max over ranks."""
+import os
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2411_10958_b200 import shard, synth
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    B, Hq, Hkv, N, d = 2, 4, 2, 64, 64
+    units = shard.rank_units(rank, world, B, Hkv)
+    qs, ks, vs = synth.make_qkv(B, Hq, Hkv, N, d, kind="structured", seed=3, units=units)
+    t = shard.max_over_ranks(1.0 + rank, world)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, units)
+    dist.destroy_process_group()
+    q.put((rank, units, t, gathered, qs.sum().item(), ks[0].numpy().copy(), vs[-1].numpy().copy()))
+
+
+def test_two_rank_sharding():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    all_units = res[0][3][0] + res[0][3][1]
+    assert len(set(all_units)) == len(all_units) == 2 * 2 * 2          # disjoint, complete
+    assert sorted(all_units) == [(b, h) for b in range(4) for h in range(2)]
+    assert res[0][2] == res[1][2] == 2.0                                # max over ranks
+    # a rank's units regenerate exactly the slice of the unsharded (global batch 4) tensors
+    qf, kf, vf = synth.make_qkv(4, 4, 2, 64, 64, kind="structured", seed=3)
+    assert (res[1][5] == kf[2, 0].numpy()).all()     # rank 1, first unit = (b=2, h=0)
+    assert (res[0][6] == vf[1, 1].numpy()).all()     # rank 0, last unit = (b=1, h=1)
+
+
+def test_split_units_balanced():
+    units = [(b, h) for b in range(3) for h in range(5)]
+    parts = [shard.split_units(units, r, 4) for r in range(4)]
+    assert sum(parts, []) == units
+    assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    with pytest.raises(ValueError):
+        shard.rank_units(2, 2, 1, 1)
