@@ -250,6 +250,11 @@ def run_ours(args, world, rank, local):
     # roofline of the dominant kernel (the tcgen05 attention kernel)
     peak, peak_src = tensor_peak()
     achieved = ops / (kms_max * 1e-3) / 1e12
+    traffic = None
+    try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[name]["dram_bytes_per_launch"]
+    except Exception:
+        pass
     # end to end through the public C ABI on host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
@@ -277,8 +282,8 @@ def run_ours(args, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
         "data": "synthetic", "config": workload_config(name),
         "gpu_launches": 5 * args.steps,
-        "roofline": {"bound": "tensor", "kernel": "k_attn (tcgen05 attention)", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+        "roofline": {"bound": "tensor", "kernel": "k_attn2 (tcgen05 attention, v1)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms_max,
                      "kernel_share_of_step": kms_max / ms_max},
         "clocks": clk.summary(),
