@@ -53,11 +53,14 @@ extern "C" {
 #define SAGE2_F_INT8 2     /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing,  */
                            /* P:70, P:476 (Table 3)                                    */
 #define SAGE2_F_KERNEL_V0 4 /* use the simple one-Q-tile-per-CTA attention kernel (A/B checks)  */
+/* Kernel variants (A/B timing and parity; the default is v6, csrc/attn6.cuh, b_kv = 128).       */
 #define SAGE2_F_KERNEL_V4 8 /* use the experimental v4 kernel (one Q tile / CTA, column-split     */
                             /* softmax warpgroups, triple-buffered S/R in TMEM)                    */
 #define SAGE2_F_DEBUG_NULLSM 16 /* v4 timing experiment: skip softmax work (output is NOT attention)*/
 #define SAGE2_F_DEBUG_NULLMMA 32 /* v4 timing experiment: skip the MMAs (output is NOT attention)   */
-#define SAGE2_F_DEBUG_TIMING 64 /* v4, sage2_debug_qk_int32 only: per-phase clock64 stamps          */
+#define SAGE2_F_DEBUG_TIMING 64 /* v1/v4, sage2_debug_qk_int32 only: per-phase clock64 stamps       */
+#define SAGE2_F_KERNEL_V1 128 /* use the v1 kernel (b_kv = 128, R written over S; A/B checks)      */
+#define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
 const char* sage2_last_cuda_error(void);

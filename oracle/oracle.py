@@ -39,7 +39,7 @@ class _Cfg(ctypes.Structure):
 class OracleConfig:
     """SageAttn2-4b defaults (Table 3): INT4 per-thread Q/K, FP8 P~ and V."""
     b_q: int = 128
-    kv_tile: int = 128
+    kv_tile: int = 128        # the kernel's b_kv (C-9): 128 (default kernel v6); 64 for v5
     causal: bool = False
     quant: bool = True
     qk_max: int = 7

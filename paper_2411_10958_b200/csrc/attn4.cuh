@@ -54,9 +54,6 @@ struct Attn4Smem {
     static constexpr uint32_t ALLOC = BYTES + 1024;
 };
 
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 template <int D, bool CAUSAL, bool DUMP, bool NULLSM = false, bool NULLMMA = false, bool TIMING = false>
 __global__ void __launch_bounds__(384, 1) k_attn4(const AttnParams p) {

@@ -1,0 +1,441 @@
+// attn5.cuh -- SageAttention2 attention kernel v5 for sm_100a (default).
+// Alg. 1 inner loop with b_kv = 64 (the paper's example block):
+// the two-level accumulation promotes a fresh 64-key partial R into the fp32 O.
+//
+// CTA = two 128-row Q blocks (i0 = 2*pair, i1 = i0 + 1) of one (b, h_q).  K^/V^ arrive in stages of
+// 128 keys (shared by both Q tiles); each stage is consumed as two 64-key sub-tiles u = 2j + hk.
+//
+// TMEM (512 columns): S0 [0,64) | S1 [64,128) | R[0] [128,192) | R[1] [192,256) | O0 | O1 (D each).
+// S and R are separate, so QK(u+1) is issued as soon as the softmax has read S(u) -- the promotion
+// of R never sits on the QK -> softmax chain.  R = P^ V^ is produced in 64-channel pieces (two for
+// d = 128) that alternate between the two R buffers, so the PV issuer runs one piece ahead of the
+// promotion.
+//
+// 16 warps (512 threads).  Single-thread roles sit in the highest warp ids (the issue arbiter
+// favours high warp ids):
+//   warps 0-3    softmax, Q tile 0 } one thread per query row (TMEM lane = row), 64 keys per step:
+//   warps 4-7    softmax, Q tile 1 }   s = S*dQ*dK*log2e/sqrt(d) + Delta S', masks, exact
+//                                      running max (C-10), P^ = e4m3(2^(s-m+log2 448)) -> smem
+//                                      (A operand of the PV MMA), row sum l.
+//                                      The exp2 phases of the two tiles alternate (named barriers
+//                                      8/9): one tile's ALU-bound dequant overlaps the other's MUFU.
+//   warps 8-11   two-level promotion O = alpha O + R in fp32 for both tiles, epilogue
+//                O / l / 448 * delta_V -> fp16
+//   warp 12      producer: bulk-async (TMA engine) copies of the pre-swizzled tile images
+//   warps 13/14  QK issuers of tile 0 / 1:  S = Q^ K^^T  tcgen05.mma.kind::i8 (exact s32)
+//   warp 15      PV issuer of both tiles:  R = P^ V^  tcgen05.mma.kind::f8f6f4 (E4M3, fresh fp32
+//                accumulator); separate from the QK issuers so QK(u+1) never waits on a promotion
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
+#include <cstdint>
+
+#include "attn.cuh"
+#include "ptx.cuh"
+
+namespace sage2 {
+
+constexpr int kStages5 = 3;
+
+template <int D>
+struct Attn5Smem {
+    static constexpr uint32_t TILE = 128 * D;
+    static constexpr uint32_t Q0 = 0, Q1 = TILE;
+    // stage (128 keys): K^ | V^T | dS tile0 (512) | dS tile1 (512) | dK (32)
+    static constexpr uint32_t ST_K = 0, ST_V = TILE, ST_DS0 = 2 * TILE, ST_DS1 = 2 * TILE + 512,
+                              ST_DK = 2 * TILE + 1024;
+    static constexpr uint32_t STAGE = ((2 * TILE + 1024 + 32) + 1023) / 1024 * 1024;
+    static constexpr uint32_t ST0 = 2 * TILE;
+    static constexpr uint32_t P = ST0 + kStages5 * STAGE;   // P^ images [tile][2] 128 x 128 e4m3
+    static constexpr uint32_t ALPHA = P + 4 * 16384;         // float [tile][4 slots][128]
+    static constexpr uint32_t LSUM = ALPHA + 2 * 4 * 128 * 4; // float [tile][128]
+    static constexpr uint32_t BAR = LSUM + 2 * 128 * 4;
+    // q_full, kv_full[S], kv_empty[S]; per tile: s_full, s_free, p_full[4], p_free[4], l_ready
+    // (11 per tile); r_full[2], r_free[2] (per R buffer)
+    static constexpr uint32_t NBAR = 1 + 2 * kStages5 + 2 * 11 + 4;
+    static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
+    static constexpr uint32_t BYTES = TMEMPTR + 16;
+    static constexpr uint32_t ALLOC = BYTES + 1024;
+};
+
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
+__global__ void __launch_bounds__(512, 1) k_attn5(const AttnParams p) {
+    using L = Attn5Smem<D>;
+    constexpr int NH = D / 64;                     // R halves of 64 channels (1 for d=64, 2 for d=128)
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int wg = warp / 4;
+    const int nT = p.nT, Np = nT * 128;
+    const int npairs = (nT + 1) / 2;
+    const int pair = CAUSAL ? (npairs - 1 - (int)blockIdx.x) : (int)blockIdx.x;   // heavy causal pairs first
+    const int hq = blockIdx.y, b = blockIdx.z;
+    const int bhq = b * p.Hq + hq;
+    const int bhk = b * p.Hkv + hq / (p.Hq / p.Hkv);
+    const int it0 = 2 * pair, it1 = 2 * pair + 1;
+    const int nkv0 = CAUSAL ? it0 + 1 : nT;                       // 128-key stages per tile
+    const int nkv1 = (it1 < nT) ? (CAUSAL ? it1 + 1 : nT) : 0;
+    const int nkv_max = nkv0 > nkv1 ? nkv0 : nkv1;
+    const int ntiles = nkv1 > 0 ? 2 : 1;
+    const int U0 = 2 * nkv0, U1 = 2 * nkv1, Umax = 2 * nkv_max;   // 64-key sub-tiles
+
+    // TIMING builds: clock64 stamps of one thread per role in CTA (0,0,0) -> (uint64*)p.s_dump
+    const bool tsel = TIMING && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    auto ts = [&](int who, int j, int k) {
+        if (TIMING && tsel && j < 64)
+            reinterpret_cast<unsigned long long*>(p.s_dump)[(who * 64 + j) * 16 + k] = clock64();
+    };
+    const uint32_t bar0 = sbase + L::BAR;
+    const uint32_t bar_q = bar0;
+    auto bar_kv_full = [&](int s) { return bar0 + 8 * (1 + s); };
+    auto bar_kv_empty = [&](int s) { return bar0 + 8 * (1 + kStages5 + s); };
+    auto tb = [&](int k, int idx) { return bar0 + 8 * (1 + 2 * kStages5 + 11 * k + idx); };
+    auto bar_s_full = [&](int k) { return tb(k, 0); };
+    auto bar_s_free = [&](int k) { return tb(k, 1); };
+    auto bar_p_full = [&](int k, int u) { return tb(k, 2 + (u & 3)); };
+    auto bar_p_free = [&](int k, int u) { return tb(k, 6 + (u & 3)); };
+    auto bar_l_ready = [&](int k) { return tb(k, 10); };
+    auto bar_r_full = [&](int rb) { return bar0 + 8 * (1 + 2 * kStages5 + 22 + rb); };
+    auto bar_r_free = [&](int rb) { return bar0 + 8 * (1 + 2 * kStages5 + 24 + rb); };
+    auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
+    // P^ slot of sub-tile u: image (u/2)%2 of tile k, key bytes 64*(u%2) .. +63 of every row
+    auto p_image = [&](int k, int u) { return L::P + (2 * k + ((u >> 1) & 1)) * 16384; };
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < kStages5; ++s) {
+            mbar_init(bar_kv_full(s), 1);
+            mbar_init(bar_kv_empty(s), 1);      // PV issuer's commit after the stage's last PVs
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(bar_s_full(k), 1);
+            mbar_init(bar_s_free(k), 128);
+            for (int u = 0; u < 4; ++u) {
+                mbar_init(bar_p_full(k, u), 128);
+                mbar_init(bar_p_free(k, u), 1);
+            }
+            mbar_init(bar_l_ready(k), 128);
+        }
+        for (int rb = 0; rb < 2; ++rb) {
+            mbar_init(bar_r_full(rb), 1);
+            mbar_init(bar_r_free(rb), 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 12) tmem_alloc<512>(sbase + L::TMEMPTR);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sgen + L::TMEMPTR);
+    float* s_alpha = reinterpret_cast<float*>(sgen + L::ALPHA);
+    float* s_lsum = reinterpret_cast<float*>(sgen + L::LSUM);
+
+    if (wg == 3) {
+        setmaxnreg_dec<56>();
+        if (warp == 12 && lane == 0) {
+            // ===================== producer =====================
+            const size_t tile_bytes = (size_t)128 * D;
+            mbar_arrive_expect_tx(bar_q, L::TILE * ntiles);
+            bulk_g2s(sbase + L::Q0, p.qhat + ((size_t)bhq * nT + it0) * tile_bytes, L::TILE, bar_q);
+            if (ntiles == 2)
+                bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)bhq * nT + it1) * tile_bytes, L::TILE, bar_q);
+            const uint64_t keep = policy_evict_last();
+            for (int j = 0; j < nkv_max; ++j) {
+                const int s = j % kStages5;
+                if (j >= kStages5) mbar_wait(bar_kv_empty(s), ((j / kStages5) - 1) & 1);
+                const uint32_t sa = stage_addr(s);
+                const bool d0 = j < nkv0, d1 = j < nkv1;
+                mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 32 + 512 * (d0 + d1));
+                bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                bulk_g2s(sa + L::ST_DK, p.dk + (size_t)bhk * nT * 8 + (size_t)j * 8, 32, bar_kv_full(s));
+                if (d0)
+                    bulk_g2s(sa + L::ST_DS0, p.ds + ((size_t)bhq * nT + it0) * Np + (size_t)j * 128, 512, bar_kv_full(s));
+                if (d1)
+                    bulk_g2s(sa + L::ST_DS1, p.ds + ((size_t)bhq * nT + it1) * Np + (size_t)j * 128, 512, bar_kv_full(s));
+            }
+        } else if ((warp == 13 || warp == 14) && lane == 0) {
+            // ===================== QK issuer for Q tile k =====================
+            // Independent of the PV side: S(u) only needs the stage and the softmax having read S(u-1).
+            const int k = warp - 13;
+            const int U = k ? U1 : U0;
+            constexpr uint32_t IDQK = idesc_i8(128, 64);
+            const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
+            const uint32_t tS = tmem + 64 * k;
+            mbar_wait(bar_q, 0);
+            for (int u = 0; u < U; ++u) {
+                const int j = u >> 1, s = j % kStages5, hk = u & 1;
+                mbar_wait(bar_kv_full(s), (j / kStages5) & 1);
+                if (u >= 1) mbar_wait(bar_s_free(k), (u - 1) & 1);      // softmax read S(u-1)
+                tc_fence_after();
+                // keys 64 hk .. of the stage: K^ rows start 64 rows = 8 core-matrix groups later
+                const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K + hk * (64 * D));
+#pragma unroll
+                for (int kk = 0; kk < D / 32; ++kk) mma_i8(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                mma_commit(bar_s_full(k));
+                ts(4 + k, u, 1);
+            }
+        } else if (warp == 15 && lane == 0) {
+            // ===================== PV issuer for both Q tiles =====================
+            constexpr uint32_t IDPV = idesc_e4m3(128, 64);
+            int q = 0;                                             // R pieces issued (R buffer = q % 2)
+            for (int u = 0; u < Umax; ++u) {
+                const int j = u >> 1, s = j % kStages5, hk = u & 1;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (u >= (k ? U1 : U0)) continue;
+                    mbar_wait(bar_p_full(k, u), (u >> 2) & 1);        // softmax wrote P^(u)
+                    tc_fence_after();
+                    ts(4 + k, u, 2);
+                    const uint64_t pdesc = smem_desc<128>(sbase + p_image(k, u)) + 4 * hk;   // K-steps 2hk, 2hk+1
+#pragma unroll
+                    for (int h = 0; h < NH; ++h, ++q) {
+                        const int rb = q & 1;
+                        if (q >= 2) mbar_wait(bar_r_free(rb), ((q >> 1) - 1) & 1);   // buffer promoted
+                        tc_fence_after();
+                        // V^T rows (channels) 64 h .. 64 h + 63: 8 core-matrix groups of 1024 B each
+                        const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V + h * 8192) + 4 * hk;
+                        const uint32_t tR = tmem + 128 + 64 * rb;
+                        mma_f8f6f4(tR, pdesc, vdesc, IDPV, 0);
+                        mma_f8f6f4(tR, pdesc + 2, vdesc + 2, IDPV, 1);
+                        mma_commit(bar_r_full(rb));
+                        ts(4 + k, u, 3 + h);
+                    }
+                    mma_commit(bar_p_free(k, u));
+                }
+                // the stage (K^ for both tiles' QK, V^ and Delta S / delta_K) is free once every PV of
+                // its second sub-tile completed (the QKs completed before the softmax produced P^)
+                if (hk == 1) mma_commit(bar_kv_empty(s));
+            }
+        }
+    } else if (wg == 0 || wg == 1) {
+        setmaxnreg_inc<152>();
+        // ===================== softmax for Q tile k =====================
+        const int k = wg;
+        const int U = k ? U1 : U0, my_it = k ? it1 : it0;
+        auto turn_wait = [&]() { named_bar_sync(8 + k, 256); };
+        auto turn_pass = [&]() { named_bar_arrive(8 + (1 - k), 256); };
+        if (k == 1) turn_pass();                    // tile 0 takes the first MUFU turn
+        if (U > 0) {
+            const int wq = warp & 3;
+            const int row = 32 * wq + lane;
+            const uint32_t tS = tmem + 64 * k + ((uint32_t)(32 * wq) << 16);
+            const int grow = my_it * 128 + row;
+            const float dqr = p.dq[((size_t)bhq * nT + my_it) * 32 + 8 * (row / 32) + (row % 8)] * p.qk_scale_log2;
+            float m = -INFINITY, l = 0.0f;
+            const bool tme = TIMING && lane == 0 && wq == 0;
+            for (int u = 0; u < U; ++u) {
+                const int j = u >> 1, s = j % kStages5, hk = u & 1;
+                if (tme) ts(k, u, 0);
+                if (hk == 0) mbar_wait(bar_kv_full(s), (j / kStages5) & 1);   // Delta S / delta_K landed
+                mbar_wait(bar_s_full(k), u & 1);
+                tc_fence_after();
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tS, r0);
+                tmem_ld32(tS + 32, r1);
+                tmem_wait_ld();
+                reg_dep32(r0);
+                reg_dep32(r1);
+                if (tme) ts(k, u, 1);
+                tc_fence_before();
+                mbar_arrive(bar_s_free(k));                        // S(u) consumed: QK(u+1) may go
+                if (DUMP) {
+                    int32_t* dst = p.s_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * hk;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        dst[c] = (int32_t)r0[c];
+                        dst[32 + c] = (int32_t)r1[c];
+                    }
+                }
+                // ---- dequant + Delta S, masks, max ----
+                const uint32_t dss = stage_addr(s) + (k ? L::ST_DS1 : L::ST_DS0) + 256 * hk;
+                const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK) + 4 * hk;
+                float sc[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) sc[g] = dqr * dks[g];
+                float sv[64];
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    const uint32_t* rr = c < 32 ? r0 : r1;
+                    const float4 d4 = lds128(dss + 4 * c);
+                    const float v0 = sc[(c % 8) / 2], v1 = sc[(c % 8) / 2 + 1];
+                    const float2 a = ffma2(make_float2((float)(int32_t)rr[c % 32], (float)(int32_t)rr[c % 32 + 1]),
+                                           make_float2(v0, v0), make_float2(d4.x, d4.y));
+                    const float2 bq = ffma2(make_float2((float)(int32_t)rr[c % 32 + 2], (float)(int32_t)rr[c % 32 + 3]),
+                                            make_float2(v1, v1), make_float2(d4.z, d4.w));
+                    sv[c] = a.x;
+                    sv[c + 1] = a.y;
+                    sv[c + 2] = bq.x;
+                    sv[c + 3] = bq.y;
+                }
+                if ((CAUSAL && j == my_it) || (j * 128 + 64 * hk + 64 > p.N)) {   // C-18
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        const int key = j * 128 + 64 * hk + c;
+                        if (key >= p.N || (CAUSAL && key > grow)) sv[c] = -INFINITY;
+                    }
+                }
+                float mx0 = m, mx1 = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    mx0 = fmax3(mx0, sv[c], sv[c + 1]);
+                    mx1 = fmax3(mx1, sv[c + 2], sv[c + 3]);
+                }
+                const float m_new = fmaxf(mx0, mx1);
+                const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
+                const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
+                if (tme) ts(k, u, 2);
+                if (u >= 4) mbar_wait(bar_p_free(k, u), ((u >> 2) - 1) & 1);   // PV(u-4) done with the slot
+                if (tme) ts(k, u, 3);
+                turn_wait();
+                if (tme) ts(k, u, 4);
+                // ---- P^ = e4m3(448 P~) -> smem, row sum ----
+                uint8_t* sP = sgen + p_image(k, u);
+                const float2 negm = make_float2(-m_use, -m_use);
+                float2 rs2 = make_float2(0.f, 0.f), rs2b = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c0 + 4 * q;
+                        const float2 x01 = fadd2(make_float2(sv[c], sv[c + 1]), negm);
+                        const float2 x23 = fadd2(make_float2(sv[c + 2], sv[c + 3]), negm);
+                        const float2 p01 = make_float2(ex2_approx(x01.x), ex2_approx(x01.y));
+                        const float2 p23 = make_float2(ex2_approx(x23.x), ex2_approx(x23.y));
+                        rs2 = fadd2(rs2, p01);
+                        rs2b = fadd2(rs2b, p23);
+                        const uint32_t lo = __nv_cvt_float2_to_fp8x2(p01, __NV_SATFINITE, __NV_E4M3);
+                        const uint32_t hi = __nv_cvt_float2_to_fp8x2(p23, __NV_SATFINITE, __NV_E4M3);
+                        w[q] = lo | (hi << 16);
+                    }
+                    *reinterpret_cast<uint4*>(sP + swz_off<128>(row, 64 * hk + c0)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    if (DUMP && p.p_dump)
+                        *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * hk + c0) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                s_alpha[(k * 4 + (u & 3)) * 128 + row] = alpha;
+                if (tme) ts(k, u, 5);
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(bar_p_full(k, u));
+                turn_pass();
+                if (tme) ts(k, u, 6);
+                l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
+                m = m_new;
+            }
+            s_lsum[k * 128 + row] = l;
+            mbar_arrive(bar_l_ready(k));
+        }
+        for (int u = U; u < Umax; ++u) {           // keep the MUFU turn protocol balanced
+            turn_wait();
+            turn_pass();
+        }
+    } else {
+        setmaxnreg_inc<152>();
+        // ===================== two-level promotion + epilogue (both tiles) =====================
+        const int wq = warp & 3;
+        const int row = 32 * wq + lane;
+        const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+        const float* dvp = p.dv + (size_t)bhk * D;
+        int q = 0;                                // R pieces promoted (same order as the PV issuer)
+        for (int u = 0; u < Umax; ++u) {
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) {
+                if (u >= (k ? U1 : U0)) continue;
+                const bool tmc = TIMING && lane == 0 && wq == 0;
+                if (tmc) ts(2 + k, u, 0);
+                mbar_wait(bar_p_full(k, u), (u >> 2) & 1);          // alpha(u) written
+                if (tmc) ts(2 + k, u, 1);
+                const float alpha = s_alpha[(k * 4 + (u & 3)) * 128 + row];
+                const float2 a2 = make_float2(alpha, alpha);
+                const uint32_t tO = tmem + 256 + D * k + lane_off;
+#pragma unroll
+                for (int h = 0; h < NH; ++h, ++q) {
+                    const int rb = q & 1;
+                    const uint32_t tR = tmem + 128 + 64 * rb + lane_off;
+                    mbar_wait(bar_r_full(rb), (q >> 1) & 1);
+                    tc_fence_after();
+                    if (tmc) ts(2 + k, u, 2 + 2 * h);
+                    tmem_wait_st();                                   // previous O stores landed
+                    uint32_t r0[32], r1[32], o0[32], o1[32];
+                    tmem_ld32(tR, r0);
+                    tmem_ld32(tR + 32, r1);
+                    if (u > 0) {
+                        tmem_ld32(tO + 64 * h, o0);
+                        tmem_ld32(tO + 64 * h + 32, o1);
+                    }
+                    tmem_wait_ld();
+                    reg_dep32(r0);
+                    reg_dep32(r1);
+                    tc_fence_before();
+                    mbar_arrive(bar_r_free(rb));                      // R piece in registers
+                    if (tmc) ts(2 + k, u, 3 + 2 * h);
+                    if (u > 0) {
+                        reg_dep32(o0);
+                        reg_dep32(o1);
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float2 v0 = ffma2(a2, make_float2(__uint_as_float(o0[c]), __uint_as_float(o0[c + 1])),
+                                                    make_float2(__uint_as_float(r0[c]), __uint_as_float(r0[c + 1])));
+                            const float2 v1 = ffma2(a2, make_float2(__uint_as_float(o1[c]), __uint_as_float(o1[c + 1])),
+                                                    make_float2(__uint_as_float(r1[c]), __uint_as_float(r1[c + 1])));
+                            o0[c] = __float_as_uint(v0.x);
+                            o0[c + 1] = __float_as_uint(v0.y);
+                            o1[c] = __float_as_uint(v1.x);
+                            o1[c + 1] = __float_as_uint(v1.y);
+                        }
+                        tmem_st32(tO + 64 * h, o0);
+                        tmem_st32(tO + 64 * h + 32, o1);
+                    } else {
+                        tmem_st32(tO + 64 * h, r0);
+                        tmem_st32(tO + 64 * h + 32, r1);
+                    }
+                }
+            }
+        }
+        tmem_wait_st();
+        // epilogue: O / l / 448 * delta_V  (l carries the 448 factor)
+#pragma unroll 1
+        for (int k = 0; k < 2; ++k) {
+            if ((k ? U1 : U0) == 0) continue;
+            mbar_wait(bar_l_ready(k), 0);
+            tc_fence_after();
+            const float inv_l = 1.0f / s_lsum[k * 128 + row];
+            const int grow = (k ? it1 : it0) * 128 + row;
+            const uint32_t tO = tmem + 256 + D * k + lane_off;
+            __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D;
+#pragma unroll
+            for (int ch = 0; ch < D / 32; ++ch) {
+                uint32_t o[32];
+                tmem_ld32(tO + ch * 32, o);
+                tmem_wait_ld();
+                reg_dep32(o);
+                if (grow < p.N) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 8) {
+                        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + ch * 32 + c));
+                        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + ch * 32 + c + 4));
+                        __half2 h0 = __floats2half2_rn(__uint_as_float(o[c]) * inv_l * d0.x, __uint_as_float(o[c + 1]) * inv_l * d0.y);
+                        __half2 h1 = __floats2half2_rn(__uint_as_float(o[c + 2]) * inv_l * d0.z, __uint_as_float(o[c + 3]) * inv_l * d0.w);
+                        __half2 h2 = __floats2half2_rn(__uint_as_float(o[c + 4]) * inv_l * d1.x, __uint_as_float(o[c + 5]) * inv_l * d1.y);
+                        __half2 h3 = __floats2half2_rn(__uint_as_float(o[c + 6]) * inv_l * d1.z, __uint_as_float(o[c + 7]) * inv_l * d1.w);
+                        *reinterpret_cast<uint4*>(orow + ch * 32 + c) =
+                            make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                       *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 12) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+}  // namespace sage2

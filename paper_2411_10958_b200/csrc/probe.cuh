@@ -237,6 +237,35 @@ __global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long*
                     "{%0,%1,%2,%3};"
                     : "+r"(c4[0]), "+r"(c4[1]), "+r"(c4[2]), "+r"(c4[3])
                     : "r"(a4[0]), "r"(a4[1]), "r"(a4[2]), "r"(a4[3]), "r"(b2[0]), "r"(b2[1]));
+        } else if (WHICH == 7) {   // F2FP e4m3x2 pack
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+                uint32_t v = __nv_cvt_float2_to_fp8x2(make_float2(f[i], f[i + 1]), __NV_SATFINITE, __NV_E4M3);
+                f[i] += __uint_as_float(v & 0x3f3f);
+            }
+        } else if (WHICH == 8) {   // 3-input max
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float r;
+                asm volatile("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(f[i]), "f"(f[(i + 1) & 7]), "f"(f[(i + 2) & 7]));
+                f[i] = r;
+            }
+        } else if (WHICH == 9) {   // the softmax element mix: I2F, FFMA2, FMNMX3, FADD2, MUFU, FADD2, F2FP
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+                float2 s2 = make_float2((float)ia[i], (float)ia[i + 1]);
+                unsigned long long a = *reinterpret_cast<unsigned long long*>(&s2), r;
+                asm volatile("fma.rn.f32x2 %0, %1, %1, %1;" : "=l"(r) : "l"(a));
+                float2 t = *reinterpret_cast<float2*>(&r);
+                float mm;
+                asm volatile("max.f32 %0, %1, %2, %3;" : "=f"(mm) : "f"(t.x), "f"(t.y), "f"(f[i]));
+                const float e0 = ex2_approx(t.x - mm), e1 = ex2_approx(t.y - mm);
+                uint32_t v = __nv_cvt_float2_to_fp8x2(make_float2(e0, e1), __NV_SATFINITE, __NV_E4M3);
+                f[i] += e0 + __uint_as_float(v & 0x3f00);
+                f[i + 1] += e1;
+                ia[i] += 1;
+                ia[i + 1] += 3;
+            }
         } else if (WHICH == 6) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -273,6 +302,9 @@ inline int run_micro(int which, int iters, double* per_clk_per_sm) {
     if (cudaMalloc(&cyc, 8) != cudaSuccess || cudaMalloc(&sink, 1024) != cudaSuccess) return -4;
     void (*kern)(int, unsigned long long*, float*) = nullptr;
     switch (which) {
+        case 7: kern = k_micro<7>; break;
+        case 8: kern = k_micro<8>; break;
+        case 9: kern = k_micro<9>; break;
         case 0: kern = k_micro<0>; break;
         case 1: kern = k_micro<1>; break;
         case 2: kern = k_micro<2>; break;
@@ -289,7 +321,8 @@ inline int run_micro(int which, int iters, double* per_clk_per_sm) {
     cudaFree(cyc);
     cudaFree(sink);
     const double per_iter_per_sm =
-        which == 0 ? 8.0 * 32 * 128 * 4            // bytes: 8 warps x 32 lanes x 128 cols x 4 B
+        which >= 7 ? 256.0 * 8                      // 8 elements per thread per iteration
+      : which == 0 ? 8.0 * 32 * 128 * 4            // bytes: 8 warps x 32 lanes x 128 cols x 4 B
       : which == 1 ? 8.0 * 32 * 128 * 4
       : which == 2 ? 256.0 * 8
       : which == 3 ? 256.0 * 8

@@ -12,6 +12,8 @@
 #include "attn.cuh"
 #include "attn2.cuh"
 #include "attn4.cuh"
+#include "attn5.cuh"
+#include "attn6.cuh"
 #include "prep.cuh"
 #include "probe.cuh"
 
@@ -113,18 +115,18 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP>
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false, bool NULLMMA = false>
 int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn2Smem<D>;
     constexpr uint32_t smem = L::ALLOC;
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(k_attn2<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(k_attn2<D, CAUSAL, DUMP, TIMING, NULLMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem) != cudaSuccess)
             return cuda_rc();
         configured = true;
     }
-    k_attn2<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
+    k_attn2<D, CAUSAL, DUMP, TIMING, NULLMMA><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
     return cuda_rc();
 }
 
@@ -161,6 +163,37 @@ int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
 
 int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st);
 
+template <int D, bool CAUSAL, bool DUMP>
+int launch_attn6_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn2Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn6<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    k_attn6<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
+    return cuda_rc();
+}
+
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
+int launch_attn5_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn5Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn5<D, CAUSAL, DUMP, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem) != cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    k_attn5<D, CAUSAL, DUMP, TIMING><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
+    return cuda_rc();
+}
+
+
 int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
                      const Layout& L, cudaStream_t st) {
     AttnParams p;
@@ -188,9 +221,39 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
         return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
     }
-    if (flags & (SAGE2_F_KERNEL_V4 | SAGE2_F_DEBUG_TIMING | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_NULLSM))
+    if ((flags & SAGE2_F_DEBUG_TIMING) && (flags & SAGE2_F_KERNEL_V1)) {
+        if (d == 64) return launch_attn2_t<64, false, false, true>(p, B, st);
+        return launch_attn2_t<128, false, false, true>(p, B, st);
+    }
+    if ((flags & SAGE2_F_DEBUG_TIMING) && (flags & SAGE2_F_KERNEL_V5)) {
+        if (d == 64) return launch_attn5_t<64, false, false, true>(p, B, st);
+        return launch_attn5_t<128, false, false, true>(p, B, st);
+    }
+    if ((flags & SAGE2_F_DEBUG_NULLMMA) && !(flags & SAGE2_F_KERNEL_V4)) {
+        if (d == 64) return launch_attn2_t<64, false, false, false, true>(p, B, st);
+        return launch_attn2_t<128, false, false, false, true>(p, B, st);
+    }
+    if (flags & (SAGE2_F_KERNEL_V4 | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_NULLSM))
         return launch_attention_v4(p, B, d, causal, s_dump != nullptr, flags, st);
-    // default: v1 -- two Q tiles per CTA, correction warpgroup, O in TMEM (attn2.cuh)
+    if (flags & SAGE2_F_KERNEL_V5) {
+        // v5 -- b_kv = 64, separate S / R / O in TMEM, separate QK and PV issuers (attn5.cuh)
+        if (s_dump) {
+            if (d == 64) return launch_attn5_t<64, false, true>(p, B, st);
+            return launch_attn5_t<128, false, true>(p, B, st);
+        }
+        if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
+        return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
+    }
+    if (!(flags & SAGE2_F_KERNEL_V1)) {
+        // default: v6 -- b_kv = 128, two Q tiles, promotion in the softmax warps, MUFU ping-pong
+        if (s_dump) {
+            if (d == 64) return launch_attn6_t<64, false, true>(p, B, st);
+            return launch_attn6_t<128, false, true>(p, B, st);
+        }
+        if (d == 64) return causal ? launch_attn6_t<64, true, false>(p, B, st) : launch_attn6_t<64, false, false>(p, B, st);
+        return causal ? launch_attn6_t<128, true, false>(p, B, st) : launch_attn6_t<128, false, false>(p, B, st);
+    }
+    // v1 -- two Q tiles per CTA, b_kv = 128, correction warpgroup, R over S (attn2.cuh)
     if (s_dump) {
         if (d == 64) return launch_attn2_t<64, false, true>(p, B, st);
         return launch_attn2_t<128, false, true>(p, B, st);
@@ -379,7 +442,7 @@ int sage2_bench_mma(int kind, int iters, double* ops_per_s) {
 int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
     int rc = check_device();
     if (rc) return rc;
-    if (which < 0 || which > 6 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
+    if (which < 0 || which > 9 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
     return run_micro(which, iters, per_clk_per_sm);
 }
 

@@ -127,10 +127,13 @@ def prepare(q, k, v, workspace, causal=False, int8=False):
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False):
-    """The tcgen05 attention kernel only, on a prepared workspace."""
-    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8), workspace.data_ptr(),
-                                 workspace.numel(), _stream()))
+KERNEL_FLAGS = {"v6": 0, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
+
+
+def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="v6"):
+    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default v6 or an A/B variant)."""
+    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8) | KERNEL_FLAGS[kernel],
+                                 workspace.data_ptr(), workspace.numel(), _stream()))
     return out
 
 
@@ -180,7 +183,8 @@ def bench_mma(kind, iters=20000):
 
 MICRO = {0: "tmem_ld_bytes_per_clk_sm", 1: "tmem_st_bytes_per_clk_sm", 2: "mufu_ex2_per_clk_sm",
          3: "i2f_per_clk_sm", 4: "ffma2_lanes_per_clk_sm", 5: "mma_sync_s4_ops_per_clk_sm",
-         6: "mma_sync_s8_ops_per_clk_sm"}
+         6: "mma_sync_s8_ops_per_clk_sm", 7: "f2fp_e4m3x2_elems_per_clk_sm", 8: "fmnmx3_per_clk_sm",
+         9: "softmax_mix_elems_per_clk_sm"}
 
 
 def microbench(which, iters=4096):

@@ -16,8 +16,8 @@ L = sage2.lib()
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ops = 4.0 * B * H * N * N * d
 res = {}
-VARIANTS = [("v1", 0), ("v4", 8), ("v0", 4), ("v4_nullsm", 16), ("v4_nullmma", 32), ("v1_causal", 1),
-            ("v4_causal", 9)]
+VARIANTS = [("v6", 0), ("v1", 128), ("v5", 512), ("v6_causal", 1), ("v5_causal", 513), ("v4", 8), ("v0", 4), ("v4_nullsm", 24), ("v4_nullmma", 40),
+            ("v1_nullmma", 160), ("v1_causal", 129), ("v4_causal", 9)]
 if len(sys.argv) > 3:
     VARIANTS = [v for v in VARIANTS if v[0] in sys.argv[3].split(",")]
 for name, fl in VARIANTS:
