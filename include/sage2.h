@@ -60,6 +60,7 @@ extern "C" {
 #define SAGE2_F_DEBUG_NULLMMA 32 /* v4 timing experiment: skip the MMAs (output is NOT attention)   */
 #define SAGE2_F_DEBUG_TIMING 64 /* v1/v4, sage2_debug_qk_int32 only: per-phase clock64 stamps       */
 #define SAGE2_F_KERNEL_V1 128 /* use the v1 kernel (b_kv = 128, R written over S; A/B checks)      */
+#define SAGE2_F_DS_SIMT 1024 /* compute Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM */
 #define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
@@ -104,9 +105,10 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
  * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][N_pad/4]), qbar(f32 [B*H_q][nT][d]),
  * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][N_pad/16]),
  * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), ds(f32 [B*H_q][nT][N_pad], scaled by
- * log2(e)/sqrt(d)), end) -- tile images are K-major, 128B (d=128) / 64B (d=64) swizzled, the exact
+ * log2(e)/sqrt(d)), qbt(q_bar tf32 big/small split images [B*H_q][ceil(nT/256)][d/32][2][256*128 B],
+ * input of the tensor-core Delta S GEMM), end) -- tile images are K-major, 128B (d=128) / 64B (d=64) swizzled, the exact
  * shared-memory image the tensor cores read.  Returns 0 or SAGE2_EINVAL. */
-#define SAGE2_WS_NREGIONS 12
+#define SAGE2_WS_NREGIONS 13
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 
 /* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */

@@ -35,6 +35,11 @@ __device__ __forceinline__ float fixed_mean(long long sum, int n) {
     return (float)__ddiv_rn(s, (double)n);
 }
 
+// fp32 -> nearest tf32 (10-bit mantissa) kept in an fp32 container; x - tf32_big(x) is exact.
+__device__ __forceinline__ float tf32_big(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
 __device__ __forceinline__ int quant_code(float x, float delta, int qmax) {
     if (delta == 0.0f) return 0;                       // all-zero group (C-5)
     float q = rintf(__fdiv_rn(x, delta));              // IEEE division, ties-to-even (C-2, C-3)
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(256) k_kv_quant(const __half* __restrict__ K, 
 template <int D>
 __global__ void __launch_bounds__(256) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int smooth_q,
                                                  int8_t* __restrict__ qhat, float* __restrict__ dq,
-                                                 float* __restrict__ qbar_out) {
+                                                 float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
@@ -224,6 +229,14 @@ __global__ void __launch_bounds__(256) k_q_quant(const __half* __restrict__ Q, i
     if (threadIdx.x < D) {
         qbar[threadIdx.x] = smooth_q ? fixed_mean((long long)csum[threadIdx.x], n) : 0.0f;   // O-5
         qbar_out[((size_t)bh * nT + tile) * D + threadIdx.x] = qbar[threadIdx.x];
+        // tf32 big/small split of q_bar for the tensor-core Delta S GEMM (dsg.cuh): image per
+        // (bh, 256-block chunk, 32-channel atom) = [big 256 x 128 B][small 256 x 128 B], SW128.
+        const int c = threadIdx.x, nch = (nT + 255) / 256, row = tile % 256;
+        uint8_t* img = qbt + (((size_t)bh * nch + tile / 256) * (D / 32) + c / 32) * (2 * 256 * 128);
+        const float big = tf32_big(qbar[c]);
+        const uint32_t off = swz_off<128>(row, (c % 32) * 4);
+        *reinterpret_cast<float*>(img + off) = big;
+        *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qbar[c], big);
     }
     __syncthreads();
     float qp[NP][8];

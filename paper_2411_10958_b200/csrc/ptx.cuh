@@ -121,6 +121,15 @@ __device__ __forceinline__ void mma_f8f6f4(uint32_t d_tmem, uint64_t a_desc, uin
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread complete.
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -131,11 +140,16 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 //  [4,6) D format (1 = F32, 2 = S32), [7,10) A format, [10,13) B format, bit 15/16 A/B major
 //  (0 = K-major), [17,23) N>>3, [24,29) M>>4.
 //  kind::i8 : A/B format 1 = signed int8.   kind::f8f6f4 : A/B format 0 = E4M3.
+//  kind::tf32 : A/B format 2 = TF32 (fp32 containers, the low 13 mantissa bits are not used).
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_e4m3(uint32_t M, uint32_t N) {
     return (1u << 4) | (0u << 7) | (0u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 // Shared-memory matrix descriptor, K-major, swizzled canonical layout:

@@ -3,6 +3,7 @@
 // kernel (attn.cuh), plus the accumulator probe and the tensor-core microbenchmark (probe.cuh).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -15,6 +16,7 @@
 #include "attn5.cuh"
 #include "attn6.cuh"
 #include "prep.cuh"
+#include "dsg.cuh"
 #include "probe.cuh"
 
 using namespace sage2;
@@ -74,6 +76,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
         BHk * (Np / 16) * 4,  // dk
         BHk * Np * d,         // vhat
         BHq * nT * Np * 4,    // ds
+        BHq * ((nT + 255) / 256) * (size_t)(d / 32) * 65536,   // qbt (q_bar tf32 split images)
     };
     Layout L;
     size_t o = 0;
@@ -85,7 +88,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
     return L;
 }
 
-enum { R_KSUM, R_VMAX, R_KBAR, R_DV, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_END };
+enum { R_KSUM, R_VMAX, R_KBAR, R_DV, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_QBT, R_END };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -107,11 +110,30 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
         reinterpret_cast<float*>(ws + L.off[R_DV]));
     k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
                                                 reinterpret_cast<float*>(ws + L.off[R_DQ]),
-                                                reinterpret_cast<float*>(ws + L.off[R_QBAR]));
+                                                reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-    k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
-                                                reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
-                                                scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]));
+    if (flags & SAGE2_F_DS_SIMT) {
+        k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
+                                                    reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
+                                                    scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]));
+        return cuda_rc();
+    }
+    static bool configured = false;
+    static int nsm = 0;
+    if (!configured) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaFuncSetAttribute(k_delta_s_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsgSmem<D>::ALLOC) !=
+                cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    const long long items = (long long)BHq * nT * ((nT + 255) / 256);
+    const int grid = (int)std::min<long long>(items, nsm);
+    k_delta_s_tc<D><<<grid, 320, DsgSmem<D>::ALLOC, st>>>(
+        k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]), ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2,
+        reinterpret_cast<float*>(ws + L.off[R_DS]));
     return cuda_rc();
 }
 

@@ -13,8 +13,8 @@ LIB_PATH = os.path.join(_HERE, "libsage2.so")
 
 F_CAUSAL = 1
 F_INT8 = 2
-WS_NREGIONS = 12
-REGIONS = ("ksum", "vmax", "kbar", "dv", "qhat", "dq", "qbar", "khat", "dk", "vhat", "ds", "end")
+WS_NREGIONS = 13
+REGIONS = ("ksum", "vmax", "kbar", "dv", "qhat", "dq", "qbar", "khat", "dk", "vhat", "ds", "qbt", "end")
 
 _lib = None
 
@@ -119,11 +119,18 @@ def attn(q, k, v, causal=False, int8=False, out=None, workspace=None):
     return out
 
 
-def prepare(q, k, v, workspace, causal=False, int8=False):
-    """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`."""
+DS_SIMT = 1024      # include/sage2.h SAGE2_F_DS_SIMT
+
+
+def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False):
+    """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`.
+
+    ds_simt=True computes Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM
+    (A/B checks)."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
-    _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8),
+    fl = flags(causal, int8) | (DS_SIMT if ds_simt else 0)
+    _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
