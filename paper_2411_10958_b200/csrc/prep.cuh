@@ -47,9 +47,40 @@ __device__ __forceinline__ int quant_code(float x, float delta, int qmax) {
     return (int)q;
 }
 
+// round(x / delta) with IEEE division semantics (C-2, C-3), without a division on the common path:
+// q0 = x * rcp(delta) is within 2 ulp of fl(x / delta) (|q| <= 128 here, so within 2^-15); when
+// q0 is more than 2^-12 away from a half-integer both round to the same integer, otherwise the
+// exact __fdiv_rn decides.  Bit-identical to quant_code().
+__device__ __forceinline__ int quant_code_fast(float x, float delta, float rdelta, int qmax) {
+    if (delta == 0.0f) return 0;                       // all-zero group (C-5)
+    const float q0 = x * rdelta;
+    float n = rintf(q0);
+    if (fabsf(q0 - n) > 0.5f - 0x1p-12f) n = rintf(__fdiv_rn(x, delta));
+    n = fminf(fmaxf(n, -(float)qmax), (float)qmax);    // clamp (C-4)
+    return (int)n;
+}
+
+// 4 int codes -> 4 signed bytes (little endian)
+__device__ __forceinline__ uint32_t pack4_s8(int a, int b, int c, int d) {
+    // cvt.pack.sat.s8.s32.b32 d, x, y, z: d = { z[15:0], sat(x), sat(y) } (y in byte 0)
+    uint32_t hi, r;
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
+    return r;
+}
+
+// Sum the int64 column partials of the lanes that hold the same 8 channels (lane % TPR).
+template <int TPR>
+__device__ __forceinline__ void warp_sum_cols(long long (&s)[8]) {
+#pragma unroll
+    for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], m);
+}
+
 // ---------------------------------------------------------------------------------------------
 // k_kv_stats: grid (row chunks, B*Hkv), 256 threads.  Each thread reads 8 consecutive channels
-// (16 B) of a token row.
+// (16 B) of a token row, four rows in flight.
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, const __half* __restrict__ V,
@@ -57,39 +88,59 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
                                                   unsigned int* __restrict__ vmax) {
     constexpr int TPR = D / 8;          // threads per row
     constexpr int RPP = 256 / TPR;      // rows per pass
+    constexpr int U = 4;                // passes in flight
     const int bh = blockIdx.y;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     const size_t base = (size_t)bh * N * D;
     const int r0 = blockIdx.x * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
     long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t vm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = r0 + rofs; r < r1; r += RPP) {
-        uint4 kk = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)r * D + cg * 8));
-        uint4 vv = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)r * D + cg * 8));
-        const uint16_t* kh = reinterpret_cast<const uint16_t*>(&kk);
-        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&vv);
+    uint32_t vm[4] = {0, 0, 0, 0};      // |V| as fp16 bits, two channels per word
+    for (int rb = r0 + rofs; rb < r1; rb += U * RPP) {
+        uint4 kk[U], vv[U];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            s[i] += fp16_fixed24(kh[i]);
-            float a = fabsf(__half2float(__ushort_as_half(vh[i])));
-            vm[i] = max(vm[i], __float_as_uint(a));     // non-negative floats order as uints
+        for (int u = 0; u < U; ++u) {
+            const int r = rb + u * RPP;
+            kk[u] = vv[u] = make_uint4(0, 0, 0, 0);
+            if (r < r1) {
+                kk[u] = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)r * D + cg * 8));
+                vv[u] = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)r * D + cg * 8));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint16_t* kh = reinterpret_cast<const uint16_t*>(&kk[u]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(kh[i]);
+            const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv[u]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], vw[i] & 0x7FFF7FFFu);   // |fp16| orders as u16
         }
     }
-    __shared__ long long ssum[256][8];
-    __shared__ uint32_t smax[256][8];
+    warp_sum_cols<TPR>(s);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        ssum[threadIdx.x][i] = s[i];
-        smax[threadIdx.x][i] = vm[i];
+    for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], __shfl_xor_sync(0xffffffffu, vm[i], m));
+    __shared__ long long ssum[8][D];
+    __shared__ uint32_t smax[8][D];
+    if (lane < TPR) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            ssum[warp][cg * 8 + i] = s[i];
+            const uint32_t h = (vm[i / 2] >> (16 * (i % 2))) & 0xFFFFu;
+            smax[warp][cg * 8 + i] = __float_as_uint(__half2float(__ushort_as_half((uint16_t)h)));
+        }
     }
     __syncthreads();
     if (threadIdx.x < D) {
-        const int c = threadIdx.x, g = c / 8, i = c % 8;
+        const int c = threadIdx.x;
         long long t = 0;
         uint32_t m = 0;
-        for (int k = 0; k < RPP; ++k) {
-            t += ssum[k * TPR + g][i];
-            m = max(m, smax[k * TPR + g][i]);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            t += ssum[w][c];
+            m = max(m, smax[w][c]);     // non-negative floats order as uints
         }
         atomicAdd(ksum + (size_t)bh * D + c, (unsigned long long)t);   // two's-complement: exact
         atomicMax(vmax + (size_t)bh * D + c, m);
@@ -98,23 +149,39 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
 
 // ---------------------------------------------------------------------------------------------
 // k_kv_quant: grid (N_pad/128, B*Hkv), 256 threads.  One 128-token tile of one KV head.
-//   K^ tile image  : [128 tokens][D bytes], K-major swizzled (row = token)
-//   V^T tile image : [D channels][128 bytes], K-major swizzled (row = channel), E4M3
+//   K^ tile image  : [128 tokens][D bytes], K-major swizzled (row = token), stored straight from
+//                    registers (each warp writes whole 128-byte rows)
+//   V^T tile image : [D channels][128 bytes], K-major swizzled (row = channel), E4M3; V is staged
+//                    in padded shared memory and read back column-wise (thread = channel pair)
 //   dk             : 8 groups per tile (g_K = 4*(t/64) + (t%8)/2)
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256) k_kv_quant(const __half* __restrict__ K, const __half* __restrict__ V,
-                                                  int N, int qk_max, const unsigned long long* __restrict__ ksum,
-                                                  const unsigned int* __restrict__ vmax, int8_t* __restrict__ khat,
-                                                  float* __restrict__ dk, uint8_t* __restrict__ vhat,
-                                                  float* __restrict__ kbar_out, float* __restrict__ dv_out) {
+__global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ K, const __half* __restrict__ V,
+                                                     int N, int qk_max, const unsigned long long* __restrict__ ksum,
+                                                     const unsigned int* __restrict__ vmax, int8_t* __restrict__ khat,
+                                                     float* __restrict__ dk, uint8_t* __restrict__ vhat,
+                                                     float* __restrict__ kbar_out, float* __restrict__ dv_out) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // passes
+    constexpr int VS = D + 8;                                       // padded V row (halves)
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
+    const int lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     __shared__ float kbar[D], dvs[D];
     __shared__ uint32_t gmax[8];
-    __shared__ __align__(1024) uint8_t simg[kTile * D];   // staging for the swizzled V^T tile
-    __shared__ __align__(1024) uint8_t kimg[kTile * D];
+    __shared__ __align__(16) __half vt[kTile * VS];
+    const size_t base = (size_t)bh * N * D;
+    uint4 kraw[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int t = tile * kTile + p * RPP + rofs;
+        kraw[p] = make_uint4(0, 0, 0, 0);
+        uint4 vv = make_uint4(0, 0, 0, 0);
+        if (t < N) {
+            kraw[p] = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)t * D + cg * 8));
+            vv = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
+        }
+        *reinterpret_cast<uint4*>(&vt[(p * RPP + rofs) * VS + cg * 8]) = vv;
+    }
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
         kbar[c] = fixed_mean((long long)ksum[(size_t)bh * D + c], N);                 // O-1
@@ -126,66 +193,66 @@ __global__ void __launch_bounds__(256) k_kv_quant(const __half* __restrict__ K, 
     }
     if (threadIdx.x < 8) gmax[threadIdx.x] = 0;
     __syncthreads();
-    const size_t base = (size_t)bh * N * D;
-    float kp[NP][8];
+    // K' = K - k_bar (O-2) and the group absmax (g_K is uniform over the 2*TPR lanes of two rows)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs, t = tile * kTile + r;
-        uint4 kk = make_uint4(0, 0, 0, 0);
-        if (t < N) kk = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)t * D + cg * 8));
-        const __half* kh = reinterpret_cast<const __half*>(&kk);
+        const __half* kh = reinterpret_cast<const __half*>(&kraw[p]);
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            kp[p][i] = (t < N) ? __fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i]) : 0.0f;  // O-2
-            m = fmaxf(m, fabsf(kp[p][i]));
-        }
-        const int g = 4 * (r / 64) + (r % 8) / 2;                                      // g_K
-        atomicMax(&gmax[g], __float_as_uint(m));
+        for (int i = 0; i < 8; ++i)
+            if (t < N) m = fmaxf(m, fabsf(__fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i])));
+#pragma unroll
+        for (int x = 1; x < 2 * TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
+        if (lane % (2 * TPR) == 0) atomicMax(&gmax[4 * (r / 64) + (r % 8) / 2], __float_as_uint(m));
     }
     __syncthreads();
-    // K codes (O-3)
+    // K codes (O-3) straight to the swizzled K^ tile image
+    int8_t* kimg = khat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const int r = p * RPP + rofs;
-        const int g = 4 * (r / 64) + (r % 8) / 2;
-        const float delta = __fdiv_rn(__uint_as_float(gmax[g]), (float)qk_max);
-        uint32_t w[2] = {0, 0};
+        const int r = p * RPP + rofs, t = tile * kTile + r;
+        const float delta = __fdiv_rn(__uint_as_float(gmax[4 * (r / 64) + (r % 8) / 2]), (float)qk_max);
+        const float rd = __frcp_rn(delta);
+        const __half* kh = reinterpret_cast<const __half*>(&kraw[p]);
+        int code[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint32_t code = (uint32_t)(uint8_t)(int8_t)quant_code(kp[p][i], delta, qk_max);
-            w[i / 4] |= code << (8 * (i % 4));
+            const float kp = (t < N) ? __fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i]) : 0.0f;
+            code[i] = quant_code_fast(kp, delta, rd, qk_max);
         }
-        *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = make_uint2(w[0], w[1]);
+        *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) =
+            make_uint2(pack4_s8(code[0], code[1], code[2], code[3]), pack4_s8(code[4], code[5], code[6], code[7]));
     }
     if (threadIdx.x < 8)
         dk[(size_t)bh * (nT * 8) + tile * 8 + threadIdx.x] =
             __fdiv_rn(__uint_as_float(gmax[threadIdx.x]), (float)qk_max);
-    // V codes (O-4), transposed into the V^T tile (row = channel, column byte = token)
+    // V codes (O-4): thread = channel pair (c, c+1) x TOK consecutive tokens -> V^T rows c, c+1
+    constexpr int NPAIR = D / 2, TOK = kTile / (256 / NPAIR);
+    const int cp = threadIdx.x % NPAIR, t0 = (threadIdx.x / NPAIR) * TOK, c = 2 * cp;
+    const float d0 = dvs[c], d1 = dvs[c + 1];
+    uint8_t* vimg = vhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const int r = p * RPP + rofs, t = tile * kTile + r;
-        uint4 vv = make_uint4(0, 0, 0, 0);
-        if (t < N) vv = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
-        const __half* vh = reinterpret_cast<const __half*>(&vv);
+    for (int tb = 0; tb < TOK; tb += 16) {
+        uint32_t w0[4], w1[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int c = cg * 8 + i;
-            const float dvc = dvs[c];
-            uint8_t code = 0;
-            if (dvc != 0.0f)
-                code = (uint8_t)__nv_cvt_float_to_fp8(__fdiv_rn(__half2float(vh[i]), dvc), __NV_SATFINITE, __NV_E4M3);
-            simg[swz_off<128>(c, r)] = code;
+        for (int q = 0; q < 4; ++q) {
+            uint32_t pr[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const __half2 h = *reinterpret_cast<const __half2*>(&vt[(t0 + tb + 4 * q + e) * VS + c]);
+                const float2 f = __half22float2(h);
+                float2 qv;
+                qv.x = d0 != 0.0f ? __fdiv_rn(f.x, d0) : 0.0f;
+                qv.y = d1 != 0.0f ? __fdiv_rn(f.y, d1) : 0.0f;
+                pr[e] = (uint32_t)__nv_cvt_float2_to_fp8x2(qv, __NV_SATFINITE, __NV_E4M3);   // lo = c, hi = c+1
+            }
+            const uint32_t x = pr[0] | (pr[1] << 16), y = pr[2] | (pr[3] << 16);
+            w0[q] = __byte_perm(x, y, 0x6420);
+            w1[q] = __byte_perm(x, y, 0x7531);
         }
-    }
-    __syncthreads();
-    // coalesced 16-byte stores of both tile images
-    const size_t tile_bytes = (size_t)kTile * D;
-    uint4* kdst = reinterpret_cast<uint4*>(khat + ((size_t)bh * nT + tile) * tile_bytes);
-    uint4* vdst = reinterpret_cast<uint4*>(vhat + ((size_t)bh * nT + tile) * tile_bytes);
-    for (int i = threadIdx.x; i < (int)(tile_bytes / 16); i += 256) {
-        kdst[i] = reinterpret_cast<const uint4*>(kimg)[i];
-        vdst[i] = reinterpret_cast<const uint4*>(simg)[i];
+        *reinterpret_cast<uint4*>(vimg + swz_off<128>(c, t0 + tb)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(vimg + swz_off<128>(c + 1, t0 + tb)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
     }
 }
 
@@ -195,81 +262,91 @@ __global__ void __launch_bounds__(256) k_kv_quant(const __half* __restrict__ K, 
 //   (g_Q = 8*(t/32) + t%8, "tokens i, 8+i, 16+i, 24+i")
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int smooth_q,
-                                                 int8_t* __restrict__ qhat, float* __restrict__ dq,
-                                                 float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
+__global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int smooth_q,
+                                                    int8_t* __restrict__ qhat, float* __restrict__ dq,
+                                                    float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     const int n = min(kTile, N - tile * kTile);          // present tokens (C-18)
-    __shared__ unsigned long long csum[D];
+    __shared__ long long part[8][D];
     __shared__ float qbar[D];
     __shared__ uint32_t gmax[32];
-    __shared__ __align__(1024) uint8_t qimg[kTile * D];
-    if (threadIdx.x < D) csum[threadIdx.x] = 0;
     if (threadIdx.x < 32) gmax[threadIdx.x] = 0;
-    __syncthreads();
     const size_t base = (size_t)bh * N * D;
     uint4 raw[NP];
-    long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs, t = tile * kTile + r;
         raw[p] = make_uint4(0, 0, 0, 0);
         if (r < n) raw[p] = __ldg(reinterpret_cast<const uint4*>(Q + base + (size_t)t * D + cg * 8));
-        const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw[p]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(h[i]);
     }
     if (smooth_q) {
+        long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) atomicAdd(&csum[cg * 8 + i], (unsigned long long)s[i]);
+        for (int p = 0; p < NP; ++p) {
+            const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw[p]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(h[i]);
+        }
+        warp_sum_cols<TPR>(s);
+        if (lane < TPR) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) part[warp][cg * 8 + i] = s[i];
+        }
     }
     __syncthreads();
     if (threadIdx.x < D) {
-        qbar[threadIdx.x] = smooth_q ? fixed_mean((long long)csum[threadIdx.x], n) : 0.0f;   // O-5
-        qbar_out[((size_t)bh * nT + tile) * D + threadIdx.x] = qbar[threadIdx.x];
+        const int c = threadIdx.x;
+        long long t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += smooth_q ? part[w][c] : 0;
+        const float qb = smooth_q ? fixed_mean(t, n) : 0.0f;   // O-5
+        qbar[c] = qb;
+        qbar_out[((size_t)bh * nT + tile) * D + c] = qb;
         // tf32 big/small split of q_bar for the tensor-core Delta S GEMM (dsg.cuh): image per
         // (bh, 256-block chunk, 32-channel atom) = [big 256 x 128 B][small 256 x 128 B], SW128.
-        const int c = threadIdx.x, nch = (nT + 255) / 256, row = tile % 256;
+        const int nch = (nT + 255) / 256, row = tile % 256;
         uint8_t* img = qbt + (((size_t)bh * nch + tile / 256) * (D / 32) + c / 32) * (2 * 256 * 128);
-        const float big = tf32_big(qbar[c]);
+        const float big = tf32_big(qb);
         const uint32_t off = swz_off<128>(row, (c % 32) * 4);
         *reinterpret_cast<float*>(img + off) = big;
-        *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qbar[c], big);
+        *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qb, big);
     }
     __syncthreads();
-    float qp[NP][8];
+    // gamma(Q) and the per-thread group absmax (row max over the TPR lanes of a row)
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
         const __half* h = reinterpret_cast<const __half*>(&raw[p]);
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            qp[p][i] = (r < n) ? __fsub_rn(__half2float(h[i]), qbar[cg * 8 + i]) : 0.0f;
-            m = fmaxf(m, fabsf(qp[p][i]));
-        }
-        atomicMax(&gmax[8 * (r / 32) + (r % 8)], __float_as_uint(m));
+        for (int i = 0; i < 8; ++i)
+            if (r < n) m = fmaxf(m, fabsf(__fsub_rn(__half2float(h[i]), qbar[cg * 8 + i])));
+#pragma unroll
+        for (int x = 1; x < TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
+        if (cg == 0) atomicMax(&gmax[8 * (r / 32) + (r % 8)], __float_as_uint(m));
     }
     __syncthreads();
+    int8_t* img = qhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
         const float delta = __fdiv_rn(__uint_as_float(gmax[8 * (r / 32) + (r % 8)]), (float)qk_max);   // O-6
-        uint32_t w[2] = {0, 0};
+        const float rd = __frcp_rn(delta);
+        const __half* h = reinterpret_cast<const __half*>(&raw[p]);
+        int code[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint32_t code = (uint32_t)(uint8_t)(int8_t)quant_code(qp[p][i], delta, qk_max);
-            w[i / 4] |= code << (8 * (i % 4));
+            const float x = (r < n) ? __fsub_rn(__half2float(h[i]), qbar[cg * 8 + i]) : 0.0f;
+            code[i] = quant_code_fast(x, delta, rd, qk_max);
         }
-        *reinterpret_cast<uint2*>(qimg + swz_off<D>(r, cg * 8)) = make_uint2(w[0], w[1]);
+        *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) =
+            make_uint2(pack4_s8(code[0], code[1], code[2], code[3]), pack4_s8(code[4], code[5], code[6], code[7]));
     }
     if (threadIdx.x < 32)
         dq[((size_t)bh * nT + tile) * 32 + threadIdx.x] = __fdiv_rn(__uint_as_float(gmax[threadIdx.x]), (float)qk_max);
-    __syncthreads();
-    uint4* dst = reinterpret_cast<uint4*>(qhat + ((size_t)bh * nT + tile) * (size_t)kTile * D);
-    for (int i = threadIdx.x; i < kTile * D / 16; i += 256) dst[i] = reinterpret_cast<const uint4*>(qimg)[i];
 }
 
 // ---------------------------------------------------------------------------------------------
