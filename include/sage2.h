@@ -58,9 +58,12 @@ extern "C" {
                             /* softmax warpgroups, triple-buffered S/R in TMEM)                    */
 #define SAGE2_F_DEBUG_NULLSM 16 /* v4 timing experiment: skip softmax work (output is NOT attention)*/
 #define SAGE2_F_DEBUG_NULLMMA 32 /* v4 timing experiment: skip the MMAs (output is NOT attention)   */
-#define SAGE2_F_DEBUG_TIMING 64 /* v1/v4, sage2_debug_qk_int32 only: per-phase clock64 stamps       */
+#define SAGE2_F_DEBUG_TIMING 64 /* sage2_debug_qk_int32 only: per-phase clock64 stamps (v1/v4/v5/v6) */
 #define SAGE2_F_KERNEL_V1 128 /* use the v1 kernel (b_kv = 128, R written over S; A/B checks)      */
 #define SAGE2_F_DS_SIMT 1024 /* compute Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM */
+#define SAGE2_F_QK_E4M3 2048 /* E4M3-carrier QK^T: INT4 codes stored as E4M3 bytes, S on kind::f8f6f4 */
+                             /* (fp32 accumulator, same integer S); pass to BOTH sage2_prepare and  */
+                             /* sage2_attention.  Invalid with SAGE2_F_INT8 or a KERNEL flag.       */
 #define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */

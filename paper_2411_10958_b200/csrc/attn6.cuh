@@ -30,7 +30,11 @@
 
 namespace sage2 {
 
-template <int D, bool CAUSAL, bool DUMP>
+// QKF8: the E4M3-carrier variant of QK^T (SAGE2_F_QK_E4M3): the INT4-range codes arrive as E4M3
+// bytes and S = Q^ K^^T runs on tcgen05.mma.kind::f8f6f4 into an fp32 accumulator; every product
+// is an integer <= 49 and |S| <= 49 d < 2^24, so S is the same integer as on kind::i8, but the
+// softmax reads it as fp32 (no I2F per score).
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false, bool QKF8 = false>
 __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
     using L = Attn2Smem<D>;                        // same shared-memory plan as v1
     extern __shared__ uint8_t smem_raw[];
@@ -51,6 +55,16 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
     const int nkv_max = nkv0 > nkv1 ? nkv0 : nkv1;
     const int ntiles = nkv1 > 0 ? 2 : 1;
 
+    // TIMING builds: clock64 stamps of one thread per role in CTA (0,0,0) -> (uint64*)p.s_dump
+    // [who][j][slot], who = softmax tile 0/1, MMA issuer 0/1 (2, 3), producer (4)
+    // S accumulator word -> value: s32 (kind::i8) or fp32 (E4M3 carrier)
+    auto s_as_float = [](uint32_t u) { return QKF8 ? __uint_as_float(u) : (float)(int32_t)u; };
+    auto s_as_int = [](uint32_t u) { return QKF8 ? (int32_t)__uint_as_float(u) : (int32_t)u; };
+    const bool tsel = TIMING && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    auto ts = [&](int who, int j, int slot) {
+        if (TIMING && tsel && j < 64 && (threadIdx.x & 31) == 0)
+            reinterpret_cast<unsigned long long*>(p.s_dump)[(who * 64 + j) * 16 + slot] = clock64();
+    };
     const uint32_t bar0 = sbase + L::BAR;
     const uint32_t bar_q = bar0;
     auto bar_kv_full = [&](int s) { return bar0 + 8 * (1 + s); };
@@ -96,6 +110,7 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 if (j >= kStages2) mbar_wait(bar_kv_empty(s), ((j / kStages2) - 1) & 1);
                 const uint32_t sa = stage_addr(s);
                 const bool d0 = j < nkv0, d1 = j < nkv1;
+                ts(4, j, 0);
                 mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 32 + 512 * (d0 + d1));
                 bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
                 bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
@@ -105,11 +120,12 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 if (d1)
                     bulk_g2s(sa + L::ST_DS1, p.ds + ((size_t)bhq * nT + it1) * Np + (size_t)j * 128, 512, bar_kv_full(s));
             }
-        } else if ((warp == 9 || warp == 10) && lane == 0) {
+        } else if (warp == 9 || warp == 10) {
             // ===================== MMA issuer for Q tile k =====================
+            // (whole warp converged, one elected lane issues: descriptors stay in uniform registers)
             const int k = warp - 9;
             const int my_nkv = k ? nkv1 : nkv0;
-            constexpr uint32_t IDQK = idesc_i8(128, 128);
+            constexpr uint32_t IDQK = QKF8 ? idesc_e4m3(128, 128) : idesc_i8(128, 128);
             constexpr uint32_t IDPV = idesc_e4m3(128, D);
             const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
             const uint64_t pdesc = smem_desc<128>(sbase + (k ? L::P1 : L::P0));
@@ -117,24 +133,34 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
             mbar_wait(bar_q, 0);
             for (int j = 0; j < nkv_max; ++j) {
                 const int s = j % kStages2;
+                ts(2 + k, j, 3);
                 mbar_wait(bar_kv_full(s), (j / kStages2) & 1);
+                ts(2 + k, j, 4);
                 if (j >= my_nkv) {                 // this tile is done: release the stage for it
-                    mbar_arrive(bar_kv_empty(s));
+                    if (lane == 0) mbar_arrive(bar_kv_empty(s));
                     continue;
                 }
                 if (j >= 1) mbar_wait(bar_s_free(k), (j - 1) & 1);   // R_k(j-1) read out of TMEM
+                ts(2 + k, j, 5);
                 tc_fence_after();
                 const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K);
 #pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk) mma_i8(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
-                mma_commit(bar_s_full(k));
+                for (int kk = 0; kk < D / 32; ++kk) {
+                    if (QKF8) mma_f8f6f4_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                    else mma_i8_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                    if (kk == 0) ts(2 + k, j, 6);
+                }
+                mma_commit_w(bar_s_full(k));
+                ts(2 + k, j, 0);
                 mbar_wait(bar_p_full(k), j & 1);                    // softmax_k(j) wrote P^_k
+                ts(2 + k, j, 1);
                 tc_fence_after();
                 const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma_f8f6f4(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
-                mma_commit(bar_r_full(k));
-                mma_commit(bar_kv_empty(s));
+                for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                mma_commit_w(bar_r_full(k));
+                mma_commit_w(bar_kv_empty(s));
+                ts(2 + k, j, 2);
             }
         }
     } else {
@@ -155,10 +181,14 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
             const float dqr = p.dq[((size_t)bhq * nT + my_it) * 32 + 8 * (row / 32) + (row % 8)] * p.qk_scale_log2;
             uint8_t* sP = sgen + (k ? L::P1 : L::P0);
             float m = -INFINITY, l = 0.0f;
+            const bool tme = TIMING && lane == 0 && wq == 0;
+            auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
             for (int j = 0; j < my_nkv; ++j) {
                 const int s = j % kStages2;
+                tss(j, 0);
                 mbar_wait(bar_kv_full(s), (j / kStages2) & 1);      // Delta S / delta_K landed
                 mbar_wait(bar_s_full(k), j & 1);
+                tss(j, 1);
                 tc_fence_after();
                 const uint32_t dss = stage_addr(s) + (k ? L::ST_DS1 : L::ST_DS0);
                 const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK);
@@ -184,10 +214,10 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                         int32_t* dst = p.s_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128;
 #pragma unroll
                         for (int c = 0; c < 32; ++c) {
-                            dst[c] = (int32_t)r0[c];
-                            dst[32 + c] = (int32_t)r1[c];
-                            dst[64 + c] = (int32_t)r2[c];
-                            dst[96 + c] = (int32_t)r3[c];
+                            dst[c] = s_as_int(r0[c]);
+                            dst[32 + c] = s_as_int(r1[c]);
+                            dst[64 + c] = s_as_int(r2[c]);
+                            dst[96 + c] = s_as_int(r3[c]);
                         }
                     }
 #pragma unroll
@@ -195,9 +225,9 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                         const uint32_t* rr = c < 32 ? r0 : c < 64 ? r1 : c < 96 ? r2 : r3;
                         const float4 d4 = lds128(dss + 4 * c);
                         const int g = (c / 64) * 4 + (c % 8) / 2;
-                        const float2 a = ffma2(make_float2((float)(int32_t)rr[c % 32], (float)(int32_t)rr[c % 32 + 1]),
+                        const float2 a = ffma2(make_float2(s_as_float(rr[c % 32]), s_as_float(rr[c % 32 + 1])),
                                                sc2[g], make_float2(d4.x, d4.y));
-                        const float2 bq = ffma2(make_float2((float)(int32_t)rr[c % 32 + 2], (float)(int32_t)rr[c % 32 + 3]),
+                        const float2 bq = ffma2(make_float2(s_as_float(rr[c % 32 + 2]), s_as_float(rr[c % 32 + 3])),
                                                 sc2[g + 1], make_float2(d4.z, d4.w));
                         sv[c] = a.x;
                         sv[c + 1] = a.y;
@@ -205,6 +235,7 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                         sv[c + 3] = bq.y;
                     }
                 }
+                tss(j, 2);
                 if ((CAUSAL && j == my_it) || (j * 128 + 128 > p.N)) {   // C-18
 #pragma unroll
                     for (int c = 0; c < 128; ++c) {
@@ -223,7 +254,9 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 const float m_new = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
                 const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
                 const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
+                tss(j, 3);
                 turn_wait();
+                tss(j, 4);
                 const float2 negm = make_float2(-m_use, -m_use);
                 float2 rs2 = make_float2(0.f, 0.f), rs2b = make_float2(0.f, 0.f);
 #pragma unroll
@@ -250,11 +283,13 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 fence_proxy_async_smem();
                 tc_fence_before();
                 mbar_arrive(bar_p_full(k));
+                tss(j, 5);
                 turn_pass();
                 l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
                 m = m_new;
                 // ---- two-level promotion O = alpha * O + R(j) ----
                 mbar_wait(bar_r_full(k), j & 1);
+                tss(j, 6);
                 tc_fence_after();
                 uint32_t r[D];
 #pragma unroll
@@ -264,6 +299,7 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 for (int c = 0; c < D; c += 32) reg_dep32(*reinterpret_cast<uint32_t(*)[32]>(&r[c]));
                 tc_fence_before();
                 mbar_arrive(bar_s_free(k));                // R in registers: QK(j+1) may overwrite S/R
+                tss(j, 7);
                 const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
                 for (int c0 = 0; c0 < D; c0 += 32) {
@@ -286,6 +322,7 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                     tmem_st32(tO + c0, o);
                 }
                 tmem_wait_st();
+                tss(j, 8);
             }
             // ---- epilogue: O / l / 448 * delta_V  (l carries the 448 factor) ----
             // (tcgen05.ld is .sync.aligned: every lane loads, only rows < N store)

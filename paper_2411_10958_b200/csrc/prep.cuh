@@ -69,6 +69,19 @@ __device__ __forceinline__ uint32_t pack4_s8(int a, int b, int c, int d) {
     return r;
 }
 
+// 4 int codes in [-7, 7] -> 4 E4M3 bytes carrying the same integers (exact: |c| <= 16 fits the
+// 3-bit mantissa).  The E4M3-carrier QK^T variant (SAGE2_F_QK_E4M3, SURVEY.md §8(a) note) feeds
+// these to tcgen05.mma.kind::f8f6f4: same products, fp32 accumulator, identical integer S.
+__device__ __forceinline__ uint32_t pack4_e4m3(int a, int b, int c, int d) {
+    const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2((float)a, (float)b), __NV_SATFINITE, __NV_E4M3);
+    const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2((float)c, (float)d), __NV_SATFINITE, __NV_E4M3);
+    return lo | (hi << 16);
+}
+__device__ __forceinline__ uint2 pack8_codes(const int (&c)[8], bool e4m3) {
+    return e4m3 ? make_uint2(pack4_e4m3(c[0], c[1], c[2], c[3]), pack4_e4m3(c[4], c[5], c[6], c[7]))
+                : make_uint2(pack4_s8(c[0], c[1], c[2], c[3]), pack4_s8(c[4], c[5], c[6], c[7]));
+}
+
 // Sum the int64 column partials of the lanes that hold the same 8 channels (lane % TPR).
 template <int TPR>
 __device__ __forceinline__ void warp_sum_cols(long long (&s)[8]) {
@@ -157,7 +170,8 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
 // ---------------------------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ K, const __half* __restrict__ V,
-                                                     int N, int qk_max, const unsigned long long* __restrict__ ksum,
+                                                     int N, int qk_max, int e4m3_codes,
+                                                     const unsigned long long* __restrict__ ksum,
                                                      const unsigned int* __restrict__ vmax, int8_t* __restrict__ khat,
                                                      float* __restrict__ dk, uint8_t* __restrict__ vhat,
                                                      float* __restrict__ kbar_out, float* __restrict__ dv_out) {
@@ -221,8 +235,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
             const float kp = (t < N) ? __fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i]) : 0.0f;
             code[i] = quant_code_fast(kp, delta, rd, qk_max);
         }
-        *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) =
-            make_uint2(pack4_s8(code[0], code[1], code[2], code[3]), pack4_s8(code[4], code[5], code[6], code[7]));
+        *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
     if (threadIdx.x < 8)
         dk[(size_t)bh * (nT * 8) + tile * 8 + threadIdx.x] =
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 //   (g_Q = 8*(t/32) + t%8, "tokens i, 8+i, 16+i, 24+i")
 // ---------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int smooth_q,
+__global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
                                                     float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;
@@ -342,8 +355,7 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
             const float x = (r < n) ? __fsub_rn(__half2float(h[i]), qbar[cg * 8 + i]) : 0.0f;
             code[i] = quant_code_fast(x, delta, rd, qk_max);
         }
-        *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) =
-            make_uint2(pack4_s8(code[0], code[1], code[2], code[3]), pack4_s8(code[4], code[5], code[6], code[7]));
+        *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
     if (threadIdx.x < 32)
         dq[((size_t)bh * nT + tile) * 32 + threadIdx.x] = __fdiv_rn(__uint_as_float(gmax[threadIdx.x]), (float)qk_max);

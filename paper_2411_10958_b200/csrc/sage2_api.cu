@@ -92,6 +92,13 @@ enum { R_KSUM, R_VMAX, R_KBAR, R_DV, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// The E4M3 carrier only holds the INT4 codes (|c| <= 7) and exists only in the default kernel.
+bool flags_ok(int flags) {
+    const int kernels = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
+                        SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING;
+    return !((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | kernels)));
+}
+
 template <int D>
 int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int Hq, int Hkv, int N, int flags,
                    uint8_t* ws, const Layout& L, cudaStream_t st) {
@@ -105,10 +112,10 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const int rows_per_cta = 512;
     k_kv_stats<D><<<dim3((N + rows_per_cta - 1) / rows_per_cta, BHk), 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax);
     k_kv_quant<D><<<dim3(nT, BHk), 256, 0, st>>>(
-        k, v, N, qk_max, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
+        k, v, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
         reinterpret_cast<float*>(ws + L.off[R_DK]), ws + L.off[R_VHAT], reinterpret_cast<float*>(ws + L.off[R_KBAR]),
         reinterpret_cast<float*>(ws + L.off[R_DV]));
-    k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
+    k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
                                                 reinterpret_cast<float*>(ws + L.off[R_DQ]),
                                                 reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
@@ -185,18 +192,18 @@ int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
 
 int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st);
 
-template <int D, bool CAUSAL, bool DUMP>
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false, bool QKF8 = false>
 int launch_attn6_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn2Smem<D>;
     constexpr uint32_t smem = L::ALLOC;
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(k_attn6<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(k_attn6<D, CAUSAL, DUMP, TIMING, QKF8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem) != cudaSuccess)
             return cuda_rc();
         configured = true;
     }
-    k_attn6<D, CAUSAL, DUMP><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
+    k_attn6<D, CAUSAL, DUMP, TIMING, QKF8><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
     return cuda_rc();
 }
 
@@ -266,8 +273,24 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
         return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
     }
+    if (flags & SAGE2_F_QK_E4M3) {
+        // v6 with the E4M3-carrier QK^T (codes written as E4M3 by sage2_prepare with the same flag)
+        if (s_dump) {
+            if (d == 64) return launch_attn6_t<64, false, true, false, true>(p, B, st);
+            return launch_attn6_t<128, false, true, false, true>(p, B, st);
+        }
+        if (d == 64)
+            return causal ? launch_attn6_t<64, true, false, false, true>(p, B, st)
+                          : launch_attn6_t<64, false, false, false, true>(p, B, st);
+        return causal ? launch_attn6_t<128, true, false, false, true>(p, B, st)
+                      : launch_attn6_t<128, false, false, false, true>(p, B, st);
+    }
     if (!(flags & SAGE2_F_KERNEL_V1)) {
         // default: v6 -- b_kv = 128, two Q tiles, promotion in the softmax warps, MUFU ping-pong
+        if (flags & SAGE2_F_DEBUG_TIMING) {
+            if (d == 64) return launch_attn6_t<64, false, false, true>(p, B, st);
+            return launch_attn6_t<128, false, false, true>(p, B, st);
+        }
         if (s_dump) {
             if (d == 64) return launch_attn6_t<64, false, true>(p, B, st);
             return launch_attn6_t<128, false, true>(p, B, st);
@@ -348,7 +371,7 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
                   void* workspace, size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
-    if (!shapes_ok(B, H_q, H_kv, N, d) || !q || !k || !v || !workspace) return SAGE2_EINVAL;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !q || !k || !v || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (reinterpret_cast<uintptr_t>(workspace) & 255)) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
@@ -365,7 +388,7 @@ int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags
                     size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
-    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out)) return SAGE2_EINVAL;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out) || !flags_ok(flags)) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     return launch_attention(out, nullptr, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
@@ -376,7 +399,7 @@ int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H
                          int flags, const void* workspace, size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
-    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace) return SAGE2_EINVAL;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     return launch_attention(out, s_int, p_hat, B, H_q, H_kv, N, d, flags & ~SAGE2_F_CAUSAL,

@@ -9,7 +9,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsage2.so")
+# SAGE2_LIB overrides the path for A/B experiments (scripts/); the default is the in-tree build.
+LIB_PATH = os.environ.get("SAGE2_LIB") or os.path.join(_HERE, "libsage2.so")
 
 F_CAUSAL = 1
 F_INT8 = 2
@@ -84,8 +85,11 @@ def _check_inputs(q, k, v):
         raise ValueError("shape mismatch: q [B,Hq,N,d], k/v [B,Hkv,N,d]")
 
 
-def flags(causal=False, int8=False):
-    return (F_CAUSAL if causal else 0) | (F_INT8 if int8 else 0)
+F_QK_E4M3 = 2048    # include/sage2.h SAGE2_F_QK_E4M3 (E4M3-carrier QK^T variant)
+
+
+def flags(causal=False, int8=False, qk_e4m3=False):
+    return (F_CAUSAL if causal else 0) | (F_INT8 if int8 else 0) | (F_QK_E4M3 if qk_e4m3 else 0)
 
 
 def workspace_bytes(B, Hq, Hkv, N, d):
@@ -102,34 +106,35 @@ def alloc_workspace(B, Hq, Hkv, N, d, device="cuda"):
     return torch.empty(workspace_bytes(B, Hq, Hkv, N, d), dtype=torch.uint8, device=device)
 
 
-def attn(q, k, v, causal=False, int8=False, out=None, workspace=None):
-    """SageAttn2 forward: q [B,Hq,N,d], k/v [B,Hkv,N,d] fp16 CUDA -> out [B,Hq,N,d] fp16."""
+def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=False):
+    """SageAttn2 forward: q [B,Hq,N,d], k/v [B,Hkv,N,d] fp16 CUDA -> out [B,Hq,N,d] fp16.
+    qk_e4m3=True runs QK^T through the E4M3 carrier (kind::f8f6f4) instead of kind::i8."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     if out is None:
         out = torch.empty_like(q)
-    if workspace is None and not int8:
+    if workspace is None and not int8 and not qk_e4m3:
         _check(lib().sage2_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
                                 int(causal), _stream()))
         return out
     if workspace is None:
         workspace = alloc_workspace(B, Hq, Hkv, N, d, q.device)
     _check(lib().sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
-                               flags(causal, int8), workspace.data_ptr(), workspace.numel(), _stream()))
+                               flags(causal, int8, qk_e4m3), workspace.data_ptr(), workspace.numel(), _stream()))
     return out
 
 
 DS_SIMT = 1024      # include/sage2.h SAGE2_F_DS_SIMT
 
 
-def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False):
+def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3=False):
     """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`.
 
     ds_simt=True computes Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM
     (A/B checks)."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
-    fl = flags(causal, int8) | (DS_SIMT if ds_simt else 0)
+    fl = flags(causal, int8, qk_e4m3) | (DS_SIMT if ds_simt else 0)
     _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
@@ -137,21 +142,23 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False):
 KERNEL_FLAGS = {"v6": 0, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
 
 
-def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="v6"):
-    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default v6 or an A/B variant)."""
-    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d, flags(causal, int8) | KERNEL_FLAGS[kernel],
+def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="v6", qk_e4m3=False):
+    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default v6 or an A/B variant;
+    qk_e4m3 must match the prepare() call)."""
+    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
+                                 flags(causal, int8, qk_e4m3) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
     return out
 
 
-def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False):
+def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False):
     """Runs the attention kernel (non-causal) and returns the raw INT32 S = Q^ K^T read from TMEM,
     [B*Hq, N_pad, N_pad] (and, with_p=True, also the P^ E4M3 codes the kernel produced)."""
     Np = (N + 127) // 128 * 128
     s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
     ph = torch.zeros((B * Hq, Np, Np), dtype=torch.uint8, device=out.device) if with_p else None
     _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
-                                      N, d, flags(False, int8), workspace.data_ptr(), workspace.numel(),
+                                      N, d, flags(False, int8, qk_e4m3), workspace.data_ptr(), workspace.numel(),
                                       _stream()))
     return (s, ph) if with_p else s
 

@@ -244,3 +244,45 @@ def test_kernel_variants(kernel, kv_tile, d, causal, N):
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
                                    OracleConfig(causal=causal, kv_tile=kv_tile), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
+
+
+@pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128)])
+def test_qk_e4m3_carrier_s_bit_exact(N, d):
+    """E4M3-carrier QK^T (SAGE2_F_QK_E4M3): the fp32 accumulator of kind::f8f6f4 over E4M3-coded
+    INT4 codes holds exactly the integer S = Q^ K^T (products <= 49, |S| <= 49 d < 2^24)."""
+    B, Hq, Hkv = 1, 2, 1
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=3)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws, qk_e4m3=True)
+    out = torch.empty_like(qg)
+    s = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, qk_e4m3=True)
+    torch.cuda.synchronize()
+    s = s.cpu().numpy()
+    kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
+    for hq in range(Hq):
+        for i in range((N + 127) // 128):
+            qb = orc.q_block(q.numpy()[0, hq, 128 * i:min(N, 128 * i + 128)])
+            ref = orc.s_int_block(qb["qhat"], kv["khat"])
+            assert np.array_equal(s[hq, 128 * i:128 * i + 128].astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal,kind", [(1, 2, 2, 384, 128, False, "iid"),
+                                                      (2, 4, 1, 300, 64, True, "structured"),
+                                                      (1, 2, 1, 1000, 128, True, "structured")])
+def test_qk_e4m3_carrier_output_parity(B, Hq, Hkv, N, d, causal, kind):
+    """Same oracle, same bar: the carrier changes only how S is accumulated, not its value."""
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=7)
+    out = sage2.attn(qg, kg, vg, causal=causal, qk_e4m3=True)
+    ref = sage2.attn(qg, kg, vg, causal=causal)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref), "carrier output differs from the kind::i8 output"
+    units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal),
+                                   debug=True)
+    _compare_out(to_np16(out).astype(np.float64), res, units, N)
+
+
+def test_qk_e4m3_rejected_with_int8():
+    q = torch.zeros((1, 1, 128, 64), dtype=torch.float16, device="cuda")
+    with pytest.raises(sage2.Sage2Error):
+        sage2.attn(q, q, q, int8=True, qk_e4m3=True)
