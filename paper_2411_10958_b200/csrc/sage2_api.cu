@@ -15,6 +15,7 @@
 #include "attn4.cuh"
 #include "attn5.cuh"
 #include "attn6.cuh"
+#include "attn8.cuh"
 #include "prep.cuh"
 #include "dsg.cuh"
 #include "probe.cuh"
@@ -207,6 +208,21 @@ int launch_attn6_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false>
+int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn8Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem) != cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
+    return cuda_rc();
+}
+
 template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn5_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn5Smem<D>;
@@ -273,6 +289,26 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
         return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
     }
+    // default for d = 128: v8 (measured 1119 vs 1059 TOPS non-causal, 1101 vs 1023 causal at C2-32K);
+    // d = 64 keeps v6 (640 vs 601): its tiles are too small to pay for the max exchange.
+    if ((flags & SAGE2_F_KERNEL_V8) || (d == 128 && !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1)))) {
+        // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
+        const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;
+        if (flags & SAGE2_F_DEBUG_TIMING) {
+            if (d == 64) return launch_attn8_t<64, false, false, false, true>(p, B, st);
+            return launch_attn8_t<128, false, false, false, true>(p, B, st);
+        }
+        if (s_dump) {
+            if (d == 64) return f8 ? launch_attn8_t<64, false, true, true>(p, B, st) : launch_attn8_t<64, false, true>(p, B, st);
+            return f8 ? launch_attn8_t<128, false, true, true>(p, B, st) : launch_attn8_t<128, false, true>(p, B, st);
+        }
+        if (d == 64) {
+            if (f8) return causal ? launch_attn8_t<64, true, false, true>(p, B, st) : launch_attn8_t<64, false, false, true>(p, B, st);
+            return causal ? launch_attn8_t<64, true, false>(p, B, st) : launch_attn8_t<64, false, false>(p, B, st);
+        }
+        if (f8) return causal ? launch_attn8_t<128, true, false, true>(p, B, st) : launch_attn8_t<128, false, false, true>(p, B, st);
+        return causal ? launch_attn8_t<128, true, false>(p, B, st) : launch_attn8_t<128, false, false>(p, B, st);
+    }
     if (flags & SAGE2_F_QK_E4M3) {
         // v6 with the E4M3-carrier QK^T (codes written as E4M3 by sage2_prepare with the same flag)
         if (s_dump) {
@@ -286,7 +322,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
                       : launch_attn6_t<128, false, false, false, true>(p, B, st);
     }
     if (!(flags & SAGE2_F_KERNEL_V1)) {
-        // default: v6 -- b_kv = 128, two Q tiles, promotion in the softmax warps, MUFU ping-pong
+        // v6 (default for d = 64) -- b_kv = 128, two Q tiles, promotion in the softmax warps, MUFU ping-pong
         if (flags & SAGE2_F_DEBUG_TIMING) {
             if (d == 64) return launch_attn6_t<64, false, false, true>(p, B, st);
             return launch_attn6_t<128, false, false, true>(p, B, st);

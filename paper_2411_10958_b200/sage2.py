@@ -139,11 +139,12 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"v6": 0, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v6": 8192, "v8": 4096, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
 
 
-def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="v6", qk_e4m3=False):
-    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default v6 or an A/B variant;
+def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False):
+    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default = v8 for d=128 and
+    v6 for d=64, or an A/B variant;
     qk_e4m3 must match the prepare() call)."""
     _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
                                  flags(causal, int8, qk_e4m3) | KERNEL_FLAGS[kernel],

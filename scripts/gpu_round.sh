@@ -18,5 +18,8 @@ if [[ $what == all || $what == ncu ]]; then
       python bench.py --config $cfg --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_attn -s 3 -c 1 -f -o gpurun_out/prof_attn_$cfg \
       python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none -k 'regex:k_kv_stats|k_kv_quant|k_q_quant|k_delta_s' -s 4 -c 4 -f \
+      -o gpurun_out/prof_prep_$cfg python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu-baseline \
+      > gpurun_out/ncu_prep.log 2>&1
 fi
 echo done

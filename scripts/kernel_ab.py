@@ -25,7 +25,8 @@ out = torch.empty_like(q)
 L = sage2.lib()
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ops = 4.0 * B * H * N * N * d
-VARIANTS = [("v6", 0), ("v6_causal", 1), ("v1", 128), ("v1_causal", 129), ("v5", 512), ("v5_causal", 513),
+VARIANTS = [("default", 0), ("v6", 8192), ("v6_causal", 8193), ("v8", 4096), ("v8_causal", 4097), ("v8f8", 4096 + 2048),
+            ("v6f8", 8192 + 2048), ("v1", 128), ("v1_causal", 129), ("v5", 512), ("v5_causal", 513),
             ("v4", 8), ("v4_causal", 9), ("v0", 4), ("v4_nullsm", 24), ("v4_nullmma", 40), ("v1_nullmma", 160)]
 if len(sys.argv) > 3 and sys.argv[3]:
     VARIANTS = [x for x in VARIANTS if x[0] in sys.argv[3].split(",")]

@@ -226,7 +226,7 @@ def test_accuracy_vs_fp32_attention():
         assert cs > min_cos, (kind, cs)
 
 
-@pytest.mark.parametrize("kernel,kv_tile", [("v6", 128), ("v1", 128), ("v5", 64), ("v4", 128), ("v0", 128)])
+@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v8", 128), ("v6", 128), ("v1", 128), ("v5", 64), ("v4", 128), ("v0", 128)])
 @pytest.mark.parametrize("d,causal,N", [(128, False, 384), (64, True, 384), (128, True, 300), (64, False, 200)])
 def test_kernel_variants(kernel, kv_tile, d, causal, N):
     """Every attention-kernel variant kept for A/B timing matches the oracle run with its b_kv (C-9).
@@ -286,3 +286,4 @@ def test_qk_e4m3_rejected_with_int8():
     q = torch.zeros((1, 1, 128, 64), dtype=torch.float16, device="cuda")
     with pytest.raises(sage2.Sage2Error):
         sage2.attn(q, q, q, int8=True, qk_e4m3=True)
+
