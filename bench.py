@@ -276,6 +276,27 @@ def run_ours(args, world, rank, local):
                "h2d_bytes_per_step": int((q.numel() + 2 * k.numel()) * 2),
                "d2h_bytes_per_step": int(oh.numel() * 2), "ms_per_step": e2e_ms,
                "api": "sage2_attn_host (C ABI, pinned host buffers)"}
+    # validation (outside every timed region): NCCL all-gather of the outputs over NVLink, rank 0
+    # re-runs each rank's first (b, h_kv) unit alone and checks the gathered slice bit for bit
+    validation = None
+    if world > 1 and not args.no_validate:
+        from paper_2411_10958_b200.shard import gather_outputs, first_unit_check
+        g0 = time.perf_counter()
+        parts = gather_outputs(out, world)
+        torch.cuda.synchronize()
+        g_ms = (time.perf_counter() - g0) * 1e3
+        bad = None
+        if rank == 0:
+            def recompute(r):
+                u0 = rank_units(r, world, B, Hkv)[0]
+                qu, ku, vu = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=0, device=dev, units=[u0])
+                return sage2.attn(qu.view(1, grp, N, d), ku.view(1, 1, N, d), vu.view(1, 1, N, d),
+                                  causal=causal)[0]
+            bad = first_unit_check(parts, recompute)
+        del parts
+        validation = {"collective": "all_gather (NCCL)", "gathered_bytes": int(out.numel() * 2 * world),
+                      "gather_ms_wall": g_ms, "ranks_mismatched": bad,
+                      "check": "rank 0 recomputes every rank's first unit alone: bitwise equal"}
     line = {
         "metric": "attention TOPS (SageAttn2-4b forward)", "value": value, "unit": "TOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -290,6 +311,8 @@ def run_ours(args, world, rank, local):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
+    if validation is not None:
+        line["validation"] = validation
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
             ops_s, o, el, blocks, thr = oracle_sample(name, budget_s=args.cpu_budget)
@@ -312,6 +335,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-validate", action="store_true", help="skip the N>1 NCCL gather validation")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

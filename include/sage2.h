@@ -68,6 +68,9 @@ extern "C" {
 #define SAGE2_F_KERNEL_V6 8192 /* force the v6 kernel for d = 128 (A/B)                             */
 #define SAGE2_F_KERNEL_V8 4096 /* use the v8 kernel (v6 with each Q tile's softmax split over two   */
                                /* warpgroups by key columns: 4 softmax warps per SM sub-partition) */
+#define SAGE2_F_SMOOTH_V 32768 /* optional smooth V (NEXT#2): V' = V - V_m before the     */
+                               /* per-channel FP8 quantization, O + V_m in the epilogue; pass to    */
+                               /* BOTH sage2_prepare and sage2_attention (default kernels only).    */
 #define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
@@ -108,14 +111,15 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
 /* ---- staged entry points (the same kernels, split so each stage can be timed / inspected) ---- */
 
 /* Workspace layout: writes SAGE2_WS_NREGIONS byte offsets into offsets[] (regions in order:
- * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]),
+ * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), vsum(int64 [B*H_kv*d], smooth V),
+ * kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]), vmean(f32 [B*H_kv*d], smooth V V_m),
  * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][N_pad/4]), qbar(f32 [B*H_q][nT][d]),
  * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][N_pad/16]),
  * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), ds(f32 [B*H_q][nT][N_pad], scaled by
  * log2(e)/sqrt(d)), qbt(q_bar tf32 big/small split images [B*H_q][ceil(nT/256)][d/32][2][256*128 B],
  * input of the tensor-core Delta S GEMM), end) -- tile images are K-major, 128B (d=128) / 64B (d=64) swizzled, the exact
  * shared-memory image the tensor cores read.  Returns 0 or SAGE2_EINVAL. */
-#define SAGE2_WS_NREGIONS 13
+#define SAGE2_WS_NREGIONS 15
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 
 /* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */

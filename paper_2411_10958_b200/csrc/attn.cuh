@@ -32,6 +32,7 @@ struct AttnParams {
     const float* dk;        // [B*Hkv][nT*8]
     const uint8_t* vhat;    // [B*Hkv][nT] V^T tile images D x 128 (E4M3)
     const float* dv;        // [B*Hkv][D]
+    const float* vmean;     // [B*Hkv][D] V_m of the optional smooth V, or null
     const float* ds;        // [B*Hq][nT][N_pad]  Delta S * log2(e)/sqrt(d)
     __half* out;            // [B][Hq][N][D]
     int32_t* s_dump;        // debug: [B*Hq][N_pad][N_pad] raw S_int (DUMP builds only)

@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
             // (tcgen05.ld is .sync.aligned: every lane loads, only rows < N store)
             const float inv_l = 1.0f / l;
             const float* dvp = p.dv + (size_t)bhk * D;
+            const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D : nullptr;   // smooth V: O + V_m
             __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D;
 #pragma unroll
             for (int c0 = 0; c0 < D; c0 += 32) {
@@ -340,10 +341,17 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                     for (int c = 0; c < 32; c += 8) {
                         const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c));
                         const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c + 4));
-                        __half2 h0 = __floats2half2_rn(__uint_as_float(o[c]) * inv_l * d0.x, __uint_as_float(o[c + 1]) * inv_l * d0.y);
-                        __half2 h1 = __floats2half2_rn(__uint_as_float(o[c + 2]) * inv_l * d0.z, __uint_as_float(o[c + 3]) * inv_l * d0.w);
-                        __half2 h2 = __floats2half2_rn(__uint_as_float(o[c + 4]) * inv_l * d1.x, __uint_as_float(o[c + 5]) * inv_l * d1.y);
-                        __half2 h3 = __floats2half2_rn(__uint_as_float(o[c + 6]) * inv_l * d1.z, __uint_as_float(o[c + 7]) * inv_l * d1.w);
+                        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 m0 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c)) : z;
+                        const float4 m1 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c + 4)) : z;
+                        __half2 h0 = __floats2half2_rn(fmaf(__uint_as_float(o[c]) * inv_l, d0.x, m0.x),
+                                                       fmaf(__uint_as_float(o[c + 1]) * inv_l, d0.y, m0.y));
+                        __half2 h1 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 2]) * inv_l, d0.z, m0.z),
+                                                       fmaf(__uint_as_float(o[c + 3]) * inv_l, d0.w, m0.w));
+                        __half2 h2 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 4]) * inv_l, d1.x, m1.x),
+                                                       fmaf(__uint_as_float(o[c + 5]) * inv_l, d1.y, m1.y));
+                        __half2 h3 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 6]) * inv_l, d1.z, m1.z),
+                                                       fmaf(__uint_as_float(o[c + 7]) * inv_l, d1.w, m1.w));
                         *reinterpret_cast<uint4*>(orow + c0 + c) =
                             make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
                                        *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));

@@ -95,10 +95,13 @@ __device__ __forceinline__ void warp_sum_cols(long long (&s)[8]) {
 // k_kv_stats: grid (row chunks, B*Hkv), 256 threads.  Each thread reads 8 consecutive channels
 // (16 B) of a token row, four rows in flight.
 // ---------------------------------------------------------------------------------------------
-template <int D>
+// SMV (optional smooth V, NEXT#2): V's column sums are accumulated instead of its absmax
+// (the absmax of V - V_m needs V_m first: k_v_absmax_smooth).
+template <int D, bool SMV = false>
 __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, const __half* __restrict__ V,
                                                   int N, int rows_per_cta, unsigned long long* __restrict__ ksum,
-                                                  unsigned int* __restrict__ vmax) {
+                                                  unsigned int* __restrict__ vmax,
+                                                  unsigned long long* __restrict__ vsum) {
     constexpr int TPR = D / 8;          // threads per row
     constexpr int RPP = 256 / TPR;      // rows per pass
     constexpr int U = 4;                // passes in flight
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
     const size_t base = (size_t)bh * N * D;
     const int r0 = blockIdx.x * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
     long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long sv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t vm[4] = {0, 0, 0, 0};      // |V| as fp16 bits, two channels per word
     for (int rb = r0 + rofs; rb < r1; rb += U * RPP) {
         uint4 kk[U], vv[U];
@@ -125,22 +129,31 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
             const uint16_t* kh = reinterpret_cast<const uint16_t*>(&kk[u]);
 #pragma unroll
             for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(kh[i]);
-            const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv[u]);
+            if (SMV) {
+                const uint16_t* vh = reinterpret_cast<const uint16_t*>(&vv[u]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], vw[i] & 0x7FFF7FFFu);   // |fp16| orders as u16
+                for (int i = 0; i < 8; ++i) sv[i] += fp16_fixed24(vh[i]);
+            } else {
+                const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv[u]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], vw[i] & 0x7FFF7FFFu);   // |fp16| orders as u16
+            }
         }
     }
     warp_sum_cols<TPR>(s);
+    if (SMV) warp_sum_cols<TPR>(sv);
 #pragma unroll
     for (int m = TPR; m < 32; m <<= 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], __shfl_xor_sync(0xffffffffu, vm[i], m));
     __shared__ long long ssum[8][D];
+    __shared__ long long svs[SMV ? 8 : 1][D];
     __shared__ uint32_t smax[8][D];
     if (lane < TPR) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             ssum[warp][cg * 8 + i] = s[i];
+            if (SMV) svs[SMV ? warp : 0][cg * 8 + i] = sv[i];
             const uint32_t h = (vm[i / 2] >> (16 * (i % 2))) & 0xFFFFu;
             smax[warp][cg * 8 + i] = __float_as_uint(__half2float(__ushort_as_half((uint16_t)h)));
         }
@@ -148,15 +161,70 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
     __syncthreads();
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
-        long long t = 0;
+        long long t = 0, tv = 0;
         uint32_t m = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
             t += ssum[w][c];
+            if (SMV) tv += svs[SMV ? w : 0][c];
             m = max(m, smax[w][c]);     // non-negative floats order as uints
         }
         atomicAdd(ksum + (size_t)bh * D + c, (unsigned long long)t);   // two's-complement: exact
-        atomicMax(vmax + (size_t)bh * D + c, m);
+        if (SMV) atomicAdd(vsum + (size_t)bh * D + c, (unsigned long long)tv);
+        else atomicMax(vmax + (size_t)bh * D + c, m);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_v_absmax_smooth (smooth V only): V_m = exact mean of V's columns (reading C-1, like
+// k_bar), then vmax[c] = max_t |fp32(V[t,c]) - V_m[c]| (the absmax delta_V is taken over, O-4 on
+// V' = V - V_m).  Same grid as k_kv_stats; block (0, bh) also writes vmean.
+// ---------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_v_absmax_smooth(const __half* __restrict__ V, int N, int rows_per_cta,
+                                                         const unsigned long long* __restrict__ vsum,
+                                                         unsigned int* __restrict__ vmax, float* __restrict__ vmean_out) {
+    constexpr int TPR = D / 8, RPP = 256 / TPR, U = 4;
+    const int bh = blockIdx.y;
+    const int lane = threadIdx.x % 32;
+    const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
+    const size_t base = (size_t)bh * N * D;
+    __shared__ float vmean[D];
+    if (threadIdx.x < D) {
+        const float m = fixed_mean((long long)vsum[(size_t)bh * D + threadIdx.x], N);
+        vmean[threadIdx.x] = m;
+        if (blockIdx.x == 0) vmean_out[(size_t)bh * D + threadIdx.x] = m;
+    }
+    __syncthreads();
+    float vm8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) vm8[i] = vmean[cg * 8 + i];
+    float mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int r0 = blockIdx.x * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
+    for (int rb = r0 + rofs; rb < r1; rb += U * RPP) {
+        uint4 vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int r = rb + u * RPP;
+            vv[u] = make_uint4(0, 0, 0, 0);
+            if (r < r1) vv[u] = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)r * D + cg * 8));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (rb + u * RPP < r1) {
+                const __half* vh = reinterpret_cast<const __half*>(&vv[u]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], fabsf(__fsub_rn(__half2float(vh[i]), vm8[i])));
+            }
+        }
+    }
+#pragma unroll
+    for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], m));
+    if (lane < TPR) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicMax(vmax + (size_t)bh * D + cg * 8 + i, __float_as_uint(mx[i]));
     }
 }
 
@@ -174,7 +242,8 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
                                                      const unsigned long long* __restrict__ ksum,
                                                      const unsigned int* __restrict__ vmax, int8_t* __restrict__ khat,
                                                      float* __restrict__ dk, uint8_t* __restrict__ vhat,
-                                                     float* __restrict__ kbar_out, float* __restrict__ dv_out) {
+                                                     float* __restrict__ kbar_out, float* __restrict__ dv_out,
+                                                     const float* __restrict__ vmean) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // passes
     constexpr int VS = D + 8;                                       // padded V row (halves)
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
@@ -244,6 +313,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     constexpr int NPAIR = D / 2, TOK = kTile / (256 / NPAIR);
     const int cp = threadIdx.x % NPAIR, t0 = (threadIdx.x / NPAIR) * TOK, c = 2 * cp;
     const float d0 = dvs[c], d1 = dvs[c + 1];
+    const float m0 = vmean ? vmean[(size_t)bh * D + c] : 0.0f, m1 = vmean ? vmean[(size_t)bh * D + c + 1] : 0.0f;
     uint8_t* vimg = vhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int tb = 0; tb < TOK; tb += 16) {
@@ -255,9 +325,10 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
             for (int e = 0; e < 4; ++e) {
                 const __half2 h = *reinterpret_cast<const __half2*>(&vt[(t0 + tb + 4 * q + e) * VS + c]);
                 const float2 f = __half22float2(h);
+                const bool pad = tile * kTile + t0 + tb + 4 * q + e >= N;   // padded token: code 0
                 float2 qv;
-                qv.x = d0 != 0.0f ? __fdiv_rn(f.x, d0) : 0.0f;
-                qv.y = d1 != 0.0f ? __fdiv_rn(f.y, d1) : 0.0f;
+                qv.x = (d0 != 0.0f && !pad) ? __fdiv_rn(__fsub_rn(f.x, m0), d0) : 0.0f;   // V' = V - V_m
+                qv.y = (d1 != 0.0f && !pad) ? __fdiv_rn(__fsub_rn(f.y, m1), d1) : 0.0f;
                 pr[e] = (uint32_t)__nv_cvt_float2_to_fp8x2(qv, __NV_SATFINITE, __NV_E4M3);   // lo = c, hi = c+1
             }
             const uint32_t x = pr[0] | (pr[1] << 16), y = pr[2] | (pr[3] << 16);

@@ -68,8 +68,10 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
     const size_t sizes[SAGE2_WS_NREGIONS - 1] = {
         BHk * d * 8,          // ksum
         BHk * d * 4,          // vmax
+        BHk * d * 8,          // vsum (smooth V)
         BHk * d * 4,          // kbar
         BHk * d * 4,          // dv
+        BHk * d * 4,          // vmean (smooth V)
         BHq * Np * d,         // qhat
         BHq * (Np / 4) * 4,   // dq
         BHq * nT * d * 4,     // qbar
@@ -89,7 +91,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
     return L;
 }
 
-enum { R_KSUM, R_VMAX, R_KBAR, R_DV, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_QBT, R_END };
+enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_QBT, R_END };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -97,6 +99,8 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 bool flags_ok(int flags) {
     const int kernels = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
                         SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING;
+    // smooth V: the epilogue "+ V_m" exists in the default kernels (v6, v8) only
+    if ((flags & SAGE2_F_SMOOTH_V) && (flags & (kernels & ~SAGE2_F_DEBUG_TIMING))) return false;
     return !((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | kernels)));
 }
 
@@ -111,11 +115,20 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
     const int rows_per_cta = 512;
-    k_kv_stats<D><<<dim3((N + rows_per_cta - 1) / rows_per_cta, BHk), 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax);
+    const bool smv = (flags & SAGE2_F_SMOOTH_V) != 0;
+    auto* vsum = reinterpret_cast<unsigned long long*>(ws + L.off[R_VSUM]);
+    auto* vmean = reinterpret_cast<float*>(ws + L.off[R_VMEAN]);
+    const dim3 sgrid((N + rows_per_cta - 1) / rows_per_cta, BHk);
+    if (smv) {
+        k_kv_stats<D, true><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
+        k_v_absmax_smooth<D><<<sgrid, 256, 0, st>>>(v, N, rows_per_cta, vsum, vmax, vmean);
+    } else {
+        k_kv_stats<D, false><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
+    }
     k_kv_quant<D><<<dim3(nT, BHk), 256, 0, st>>>(
         k, v, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
         reinterpret_cast<float*>(ws + L.off[R_DK]), ws + L.off[R_VHAT], reinterpret_cast<float*>(ws + L.off[R_KBAR]),
-        reinterpret_cast<float*>(ws + L.off[R_DV]));
+        reinterpret_cast<float*>(ws + L.off[R_DV]), smv ? vmean : nullptr);
     k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
                                                 reinterpret_cast<float*>(ws + L.off[R_DQ]),
                                                 reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
@@ -248,6 +261,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.dk = reinterpret_cast<const float*>(ws + L.off[R_DK]);
     p.vhat = ws + L.off[R_VHAT];
     p.dv = reinterpret_cast<const float*>(ws + L.off[R_DV]);
+    p.vmean = (flags & SAGE2_F_SMOOTH_V) ? reinterpret_cast<const float*>(ws + L.off[R_VMEAN]) : nullptr;
     p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
     p.out = reinterpret_cast<__half*>(out);
     p.s_dump = s_dump;

@@ -31,3 +31,27 @@ def max_over_ranks(x, world, device=None):
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_outputs(out, world):
+    """Validation only (never on the hot path): all-gather every rank's output tensor (NCCL over
+    NVLink on the GPU box, gloo in the CPU tests).  Returns the list [out_rank0, ..., out_rank{w-1}]."""
+    if world == 1:
+        return [out]
+    import torch.distributed as dist
+    parts = [torch.empty_like(out) for _ in range(world)]
+    dist.all_gather(parts, out.contiguous())
+    return parts
+
+
+def first_unit_check(parts, recompute):
+    """Rank-0 validation of a gather: for every rank r, `recompute(r)` re-runs that rank's first
+    (b, h_kv) unit from its regenerated inputs and returns [group, N, d]; the gathered output of
+    that unit must be bitwise identical (the path is deterministic and units are independent).
+    Returns the list of ranks that mismatched."""
+    bad = []
+    for r, o in enumerate(parts):
+        ref = recompute(r)
+        if not torch.equal(o[0, : ref.shape[0]].to(ref.device), ref):
+            bad.append(r)
+    return bad

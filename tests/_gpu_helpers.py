@@ -39,6 +39,7 @@ def read_prepared(ws, lay, B, Hq, Hkv, N, d):
     out = {}
     out["kbar"] = region(ws, lay, "kbar", np.float32, B * Hkv * d).reshape(B * Hkv, d)
     out["dv"] = region(ws, lay, "dv", np.float32, B * Hkv * d).reshape(B * Hkv, d)
+    out["vmean"] = region(ws, lay, "vmean", np.float32, B * Hkv * d).reshape(B * Hkv, d)
     out["qbar"] = region(ws, lay, "qbar", np.float32, B * Hq * nT * d).reshape(B * Hq, nT, d)
     out["dq"] = region(ws, lay, "dq", np.float32, B * Hq * Np // 4).reshape(B * Hq, Np // 4)
     out["dk"] = region(ws, lay, "dk", np.float32, B * Hkv * Np // 16).reshape(B * Hkv, Np // 16)

@@ -287,3 +287,35 @@ def test_qk_e4m3_rejected_with_int8():
     with pytest.raises(sage2.Sage2Error):
         sage2.attn(q, q, q, int8=True, qk_e4m3=True)
 
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d", [(1, 2, 1, 300, 64), (2, 4, 2, 384, 128)])
+def test_smooth_v_preprocess_bit_exact(B, Hq, Hkv, N, d):
+    """Optional smooth V (SAGE2_F_SMOOTH_V): V_m, delta_V of V - V_m and the V^ codes
+    match the oracle bit for bit (exact means, reading C-1; fp32 subtract; IEEE division)."""
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured")
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws, smooth_v=True)
+    torch.cuda.synchronize()
+    g = read_prepared(ws, sage2.layout(B, Hq, Hkv, N, d), B, Hq, Hkv, N, d)
+    cfg = OracleConfig(smooth_v=True)
+    for b in range(B):
+        for hk in range(Hkv):
+            kv = orc.kv_head(k.numpy()[b, hk], v.numpy()[b, hk], cfg)
+            u = b * Hkv + hk
+            assert np.array_equal(g["vmean"][u].view(np.uint32), kv["vmean"].view(np.uint32))
+            assert np.array_equal(g["dv"][u].view(np.uint32), kv["dv"].view(np.uint32))
+            assert np.array_equal(g["vhat"][u], kv["vhat"])
+            assert np.array_equal(g["khat"][u], kv["khat"])
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(1, 2, 1, 300, 64, False), (1, 2, 2, 384, 128, True),
+                                                 (2, 4, 1, 1000, 128, False)])
+def test_smooth_v_output_parity(B, Hq, Hkv, N, d, causal):
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=5)
+    out = sage2.attn(qg, kg, vg, causal=causal, smooth_v=True)
+    torch.cuda.synchronize()
+    units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
+                                   OracleConfig(causal=causal, smooth_v=True), debug=True)
+    _compare_out(to_np16(out).astype(np.float64), res, units, N)

@@ -179,3 +179,37 @@ def test_quantized_accuracy_iid(orc):
     assert orc.cos_sim(ref, O) > 0.97          # INT4 on pure noise: measured 0.978
     O8 = _oracle_head(orc, Q, K, V, OracleConfig(qk_max=127))
     assert orc.cos_sim(ref, O8) > 0.999        # INT8 (SageAttn2-8b) is more accurate
+
+
+def test_smooth_v_constant_v_is_exact(orc):
+    """Smooth V with V constant over tokens: V' = V - V_m = 0, so delta_V = 0, every
+    V^ code is 0 and O = V_m = the V row exactly, whatever Q, K and the quantization of P do.
+    Without smoothing the same V goes through E4M3 and is only approximated."""
+    N, d = 300, 64
+    row = rnd((1, d), 90, 3.0, 5.0)
+    V = np.repeat(row, N, axis=0)
+    Q, K = rnd((N, d), 91), rnd((N, d), 92)
+    for causal in (False, True):
+        O = _oracle_head(orc, Q, K, V, OracleConfig(smooth_v=True, causal=causal))
+        assert np.array_equal(O, np.repeat(row.astype(np.float64), N, axis=0))
+    O = _oracle_head(orc, Q, K, V, OracleConfig(smooth_v=False))
+    assert not np.array_equal(O, np.repeat(row.astype(np.float64), N, axis=0))
+
+
+def test_smooth_v_helps_channel_biased_v(orc):
+    """Direction of P:798-799 (CosSim 98.25% -> 99.75% on a CogVideoX tensor): with a large
+    per-channel bias on V (U(8, 9) on a quarter of the channels), smoothing V brings the
+    quantized output closer to exact attention."""
+    N, d = 512, 64
+    g = np.random.default_rng(93)
+    Q = g.standard_normal((N, d)).astype(np.float16)
+    K = g.standard_normal((N, d)).astype(np.float16)
+    bias = np.zeros(d)
+    bias[g.permutation(d)[: d // 4]] = g.uniform(8, 9, d // 4)
+    V = (g.standard_normal((N, d)) * 0.5 + bias).astype(np.float16)
+    ref = dense_attention(Q, K, V, False)
+    err = {}
+    for sv in (False, True):
+        O = _oracle_head(orc, Q, K, V, OracleConfig(smooth_v=sv))
+        err[sv] = orc.rmse(ref, O)
+    assert err[True] < err[False]

@@ -20,8 +20,15 @@ def _worker(rank, world, port, q):
     t = shard.max_over_ranks(1.0 + rank, world)
     gathered = [None] * world
     dist.all_gather_object(gathered, units)
+    # validation gather of the per-rank outputs (here: a stand-in [B, Hq, N, d] tensor per rank)
+    out = qs.view(B, Hq, N, d).float() + rank
+    parts = shard.gather_outputs(out, world)
+    def recompute(r):    # rank r's first unit, regenerated from its seed (what bench.py's rank 0 does)
+        u0 = shard.rank_units(r, world, B, Hkv)[0]
+        return synth.make_qkv(B, Hq, Hkv, N, d, kind="structured", seed=3, units=[u0])[0][0].float() + r
+    bad = shard.first_unit_check(parts, recompute)
     dist.destroy_process_group()
-    q.put((rank, units, t, gathered, qs.sum().item(), ks[0].numpy().copy(), vs[-1].numpy().copy()))
+    q.put((rank, units, t, gathered, qs.sum().item(), ks[0].numpy().copy(), vs[-1].numpy().copy(), bad))
 
 
 def test_two_rank_sharding():
@@ -39,6 +46,7 @@ def test_two_rank_sharding():
     assert len(set(all_units)) == len(all_units) == 2 * 2 * 2          # disjoint, complete
     assert sorted(all_units) == [(b, h) for b in range(4) for h in range(2)]
     assert res[0][2] == res[1][2] == 2.0                                # max over ranks
+    assert res[0][7] == [] and res[1][7] == []                          # gathered parts in rank order
     # a rank's units regenerate exactly the slice of the unsharded (global batch 4) tensors
     qf, kf, vf = synth.make_qkv(4, 4, 2, 64, 64, kind="structured", seed=3)
     assert (res[1][5] == kf[2, 0].numpy()).all()     # rank 1, first unit = (b=2, h=0)
