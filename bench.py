@@ -25,16 +25,17 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (B, H_q, H_kv, N, d, causal, kind)
-    "c2_32k_d128": (4, 32, 32, 32768, 128, False, "iid"),
-    "c2_32k_d128_causal": (4, 32, 32, 32768, 128, True, "iid"),
-    "c2_32k_d64": (4, 32, 32, 32768, 64, False, "iid"),
-    "c2_16k_d128": (4, 32, 32, 16384, 128, False, "iid"),
-    "c2_4k_d128": (4, 32, 32, 4096, 128, False, "iid"),
-    "c2_1k_d128": (4, 32, 32, 1024, 128, False, "iid"),
+    "c1_256_d64": (1, 1, 1, 256, 64, False, "structured"),
     "c3_cogvideox": (1, 48, 48, 17776, 64, False, "structured"),
     "c4_llama_gqa": (1, 32, 8, 100000, 128, True, "iid"),
     "c5_b8": (8, 32, 32, 32768, 128, False, "iid"),
 }
+# C2 kernel sweep (BASELINE.json configs[1]): B=4, H=32, d in {64, 128}, N in {1K, 4K, 16K, 32K},
+# causal and non-causal, N(0,1) inputs (the paper's kernel-benchmark protocol)
+for _n, _tag in ((1024, "1k"), (4096, "4k"), (16384, "16k"), (32768, "32k")):
+    for _d in (64, 128):
+        for _c in (False, True):
+            CONFIGS[f"c2_{_tag}_d{_d}" + ("_causal" if _c else "")] = (4, 32, 32, _n, _d, _c, "iid")
 DEFAULT = "c2_32k_d128"
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_BF16_TFLOPS = 1590.0          # B200_PROFILING.md fallback (burst)

@@ -29,6 +29,16 @@ __device__ __forceinline__ long long fp16_fixed24(uint16_t h) {
     return (h & 0x8000) ? -v : v;
 }
 
+// fp16 -> fp64 (exact).  Sums of up to 2^29 / 65504 fp16 values in fp64 are exact in any order:
+// every value is a multiple of 2^-24 below 2^16, so a partial sum of k values needs at most
+// 40 + log2(k) bits (<= 53 for k <= 8192).  The kernels sum in fp64 within a CTA and convert the
+// exact total to the int64 fixed point of reading C-1 for the cross-CTA atomics.
+__device__ __forceinline__ double fp16_to_f64(uint16_t h) {
+    double r;
+    asm("{\n\t.reg .f16 t;\n\tmov.b16 t, %1;\n\tcvt.f64.f16 %0, t;\n\t}" : "=d"(r) : "h"(h));
+    return r;
+}
+
 // mean = fp32( fp64(sum * 2^-24) / n )   (reading C-1; identical op sequence in the oracle)
 __device__ __forceinline__ float fixed_mean(long long sum, int n) {
     double s = __dmul_rn((double)sum, 0x1p-24);
@@ -110,8 +120,8 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     const size_t base = (size_t)bh * N * D;
     const int r0 = blockIdx.x * rows_per_cta, r1 = min(N, r0 + rows_per_cta);
-    long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long sv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};     // exact (<= 512 rows per CTA, see fp16_to_f64)
+    double sv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t vm[4] = {0, 0, 0, 0};      // |V| as fp16 bits, two channels per word
     for (int rb = r0 + rofs; rb < r1; rb += U * RPP) {
         uint4 kk[U], vv[U];
@@ -128,11 +138,11 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
         for (int u = 0; u < U; ++u) {
             const uint16_t* kh = reinterpret_cast<const uint16_t*>(&kk[u]);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(kh[i]);
+            for (int i = 0; i < 8; ++i) s[i] += fp16_to_f64(kh[i]);
             if (SMV) {
                 const uint16_t* vh = reinterpret_cast<const uint16_t*>(&vv[u]);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) sv[i] += fp16_fixed24(vh[i]);
+                for (int i = 0; i < 8; ++i) sv[i] += fp16_to_f64(vh[i]);
             } else {
                 const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv[u]);
 #pragma unroll
@@ -140,14 +150,19 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
             }
         }
     }
-    warp_sum_cols<TPR>(s);
-    if (SMV) warp_sum_cols<TPR>(sv);
+#pragma unroll
+    for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            s[i] += __shfl_xor_sync(0xffffffffu, s[i], m);
+            if (SMV) sv[i] += __shfl_xor_sync(0xffffffffu, sv[i], m);
+        }
 #pragma unroll
     for (int m = TPR; m < 32; m <<= 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) vm[i] = __vmaxu2(vm[i], __shfl_xor_sync(0xffffffffu, vm[i], m));
-    __shared__ long long ssum[8][D];
-    __shared__ long long svs[SMV ? 8 : 1][D];
+    __shared__ double ssum[8][D];
+    __shared__ double svs[SMV ? 8 : 1][D];
     __shared__ uint32_t smax[8][D];
     if (lane < TPR) {
 #pragma unroll
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
     __syncthreads();
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
-        long long t = 0, tv = 0;
+        double t = 0, tv = 0;
         uint32_t m = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
@@ -169,8 +184,9 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
             if (SMV) tv += svs[SMV ? w : 0][c];
             m = max(m, smax[w][c]);     // non-negative floats order as uints
         }
-        atomicAdd(ksum + (size_t)bh * D + c, (unsigned long long)t);   // two's-complement: exact
-        if (SMV) atomicAdd(vsum + (size_t)bh * D + c, (unsigned long long)tv);
+        // exact totals -> int64 fixed point (x 2^24, exact) -> order-independent atomics
+        atomicAdd(ksum + (size_t)bh * D + c, (unsigned long long)__double2ll_rn(t * 0x1p24));
+        if (SMV) atomicAdd(vsum + (size_t)bh * D + c, (unsigned long long)__double2ll_rn(tv * 0x1p24));
         else atomicMax(vmax + (size_t)bh * D + c, m);
     }
 }
@@ -344,20 +360,28 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 // k_q_quant: grid (N_pad/128, B*Hq), 256 threads.  One 128-token Q block (= smoothing block).
 //   qbar [nT][D] fp32, Q^ tile image [128][D] swizzled, dq: 32 groups per block
 //   (g_Q = 8*(t/32) + t%8, "tokens i, 8+i, 16+i, 24+i")
+// Thread (cg, rofs) holds channels [8cg, 8cg+8) of rows rofs + RPP*p.  Instruction-lean form:
+//  * exact means in fp64: 128 fp16 values are multiples of 2^-24 below 2^23 in magnitude, so every
+//    partial sum fits 47 bits and the fp64 sum is exact in any order -- bit-identical to the int64
+//    fixed-point sum of reading C-1 (and 8x fewer instructions than the fixed-point conversion);
+//  * the group absmax without atomics: a thread's rows of one group are combined in registers, the
+//    (2 or 4) contributing threads of a group write disjoint slots of gpart;
+//  * gamma(Q) is computed once and kept in registers for the quantizer.
 // ---------------------------------------------------------------------------------------------
+
 template <int D>
 __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
                                                     float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
-    constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;
+    constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // d=128: 16 / 16 / 8; d=64: 8 / 32 / 4
+    constexpr int NSLOT = RPP / 8;                                   // contributors per group (2 / 4)
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     const int n = min(kTile, N - tile * kTile);          // present tokens (C-18)
-    __shared__ long long part[8][D];
+    __shared__ double part[8][D];
     __shared__ float qbar[D];
-    __shared__ uint32_t gmax[32];
-    if (threadIdx.x < 32) gmax[threadIdx.x] = 0;
+    __shared__ float gpart[32][4];
     const size_t base = (size_t)bh * N * D;
     uint4 raw[NP];
 #pragma unroll
@@ -367,14 +391,17 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
         if (r < n) raw[p] = __ldg(reinterpret_cast<const uint4*>(Q + base + (size_t)t * D + cg * 8));
     }
     if (smooth_q) {
-        long long s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const uint16_t* h = reinterpret_cast<const uint16_t*>(&raw[p]);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s[i] += fp16_fixed24(h[i]);
+            for (int i = 0; i < 8; ++i) s[i] += fp16_to_f64(h[i]);          // exact (see above)
         }
-        warp_sum_cols<TPR>(s);
+#pragma unroll
+        for (int m = TPR; m < 32; m <<= 1)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], m);
         if (lane < TPR) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) part[warp][cg * 8 + i] = s[i];
@@ -383,10 +410,10 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
     __syncthreads();
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
-        long long t = 0;
+        double t = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) t += smooth_q ? part[w][c] : 0;
-        const float qb = smooth_q ? fixed_mean(t, n) : 0.0f;   // O-5
+        for (int w = 0; w < 8; ++w) t += smooth_q ? part[w][c] : 0.0;
+        const float qb = smooth_q ? (float)__ddiv_rn(t, (double)n) : 0.0f;   // O-5 (= fixed_mean of C-1)
         qbar[c] = qb;
         qbar_out[((size_t)bh * nT + tile) * D + c] = qb;
         // tf32 big/small split of q_bar for the tensor-core Delta S GEMM (dsg.cuh): image per
@@ -399,37 +426,56 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
         *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qb, big);
     }
     __syncthreads();
-    // gamma(Q) and the per-thread group absmax (row max over the TPR lanes of a row)
+    // gamma(Q) (O-5) kept in registers; absmax per row (over the TPR lanes of the row), then per
+    // group over this thread's rows of the group (rows p with equal p / (NP/4))
+    float x[NP][8];
+    float qv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[i] = qbar[cg * 8 + i];
+    float gm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const __half* h = reinterpret_cast<const __half*>(&raw[p]);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&raw[p]);
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (r < n) m = fmaxf(m, fabsf(__fsub_rn(__half2float(h[i]), qbar[cg * 8 + i])));
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(h2[i]);
+            x[p][2 * i] = (r < n) ? __fsub_rn(f.x, qv[2 * i]) : 0.0f;
+            x[p][2 * i + 1] = (r < n) ? __fsub_rn(f.y, qv[2 * i + 1]) : 0.0f;
+            m = fmax3(m, fabsf(x[p][2 * i]), fabsf(x[p][2 * i + 1]));
+        }
 #pragma unroll
-        for (int x = 1; x < TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
-        if (cg == 0) atomicMax(&gmax[8 * (r / 32) + (r % 8)], __float_as_uint(m));
+        for (int o = 1; o < TPR; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        gm[p / (NP / 4)] = fmaxf(gm[p / (NP / 4)], m);
+    }
+    // group of (p, rofs): 8 * (r / 32) + r % 8 with r / 32 = p / (NP / 4), r % 8 = rofs % 8
+    if (cg == 0) {
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) gpart[8 * c4 + rofs % 8][rofs / 8] = gm[c4];
     }
     __syncthreads();
     int8_t* img = qhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const float delta = __fdiv_rn(__uint_as_float(gmax[8 * (r / 32) + (r % 8)]), (float)qk_max);   // O-6
+        const int g = 8 * (r / 32) + (r % 8);
+        float amax = gpart[g][0];
+#pragma unroll
+        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[g][k]);
+        const float delta = __fdiv_rn(amax, (float)qk_max);   // O-6
         const float rd = __frcp_rn(delta);
-        const __half* h = reinterpret_cast<const __half*>(&raw[p]);
         int code[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float x = (r < n) ? __fsub_rn(__half2float(h[i]), qbar[cg * 8 + i]) : 0.0f;
-            code[i] = quant_code_fast(x, delta, rd, qk_max);
-        }
+        for (int i = 0; i < 8; ++i) code[i] = quant_code_fast(x[p][i], delta, rd, qk_max);
         *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
-    if (threadIdx.x < 32)
-        dq[((size_t)bh * nT + tile) * 32 + threadIdx.x] = __fdiv_rn(__uint_as_float(gmax[threadIdx.x]), (float)qk_max);
+    if (threadIdx.x < 32) {
+        float amax = gpart[threadIdx.x][0];
+#pragma unroll
+        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[threadIdx.x][k]);
+        dq[((size_t)bh * nT + tile) * 32 + threadIdx.x] = __fdiv_rn(amax, (float)qk_max);
+    }
 }
 
 // ---------------------------------------------------------------------------------------------
