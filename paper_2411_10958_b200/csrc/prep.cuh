@@ -70,6 +70,31 @@ __device__ __forceinline__ int quant_code_fast(float x, float delta, float rdelt
     return (int)n;
 }
 
+// Eight codes at once: the fast reciprocal path for all, then ONE (rarely taken) branch that redoes
+// the whole group with IEEE division when any quotient lies within 2^-12 of a rounding midpoint.
+// Bit-identical to quant_code() element by element.
+__device__ __forceinline__ void quant_codes8(const float (&x)[8], float delta, float rdelta, int qmax, int (&code)[8]) {
+    if (delta == 0.0f) {                               // all-zero group (C-5)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) code[i] = 0;
+        return;
+    }
+    bool slow = false;
+    float n[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float q0 = x[i] * rdelta;
+        n[i] = rintf(q0);
+        slow |= fabsf(q0 - n[i]) > 0.5f - 0x1p-12f;
+    }
+    if (slow) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) n[i] = rintf(__fdiv_rn(x[i], delta));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) code[i] = (int)fminf(fmaxf(n[i], -(float)qmax), (float)qmax);   // clamp (C-4)
+}
+
 // 4 int codes -> 4 signed bytes (little endian)
 __device__ __forceinline__ uint32_t pack4_s8(int a, int b, int c, int d) {
     // cvt.pack.sat.s8.s32.b32 d, x, y, z: d = { z[15:0], sat(x), sat(y) } (y in byte 0)
@@ -266,7 +291,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     const int lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     __shared__ float kbar[D], dvs[D];
-    __shared__ uint32_t gmax[8];
+    __shared__ float gpart[8][4];
     __shared__ __align__(16) __half vt[kTile * VS];
     const size_t base = (size_t)bh * N * D;
     uint4 kraw[NP];
@@ -290,45 +315,64 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
             dv_out[(size_t)bh * D + c] = dvs[c];
         }
     }
-    if (threadIdx.x < 8) gmax[threadIdx.x] = 0;
     __syncthreads();
-    // K' = K - k_bar (O-2) and the group absmax (g_K is uniform over the 2*TPR lanes of two rows)
+    // K' = K - k_bar (O-2), kept in registers; row-pair absmax over the 2*TPR lanes of two rows,
+    // then per group g_K = 4*(r/64) + (r%8)/2 over this leader's passes of the group: leader L =
+    // rofs/2 owns rows 2L, 2L+1 of every pass, group (p*RPP/64, L%4); the RPP/8 leaders of a group
+    // write disjoint slots of gpart (no atomics)
+    float kx[NP][8];
+    float kb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kb[i] = kbar[cg * 8 + i];
+    float gm[2] = {0.f, 0.f};
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const int r = p * RPP + rofs, t = tile * kTile + r;
-        const __half* kh = reinterpret_cast<const __half*>(&kraw[p]);
+        const int t = tile * kTile + p * RPP + rofs;
+        const __half2* kh2 = reinterpret_cast<const __half2*>(&kraw[p]);
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (t < N) m = fmaxf(m, fabsf(__fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i])));
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(kh2[i]);
+            kx[p][2 * i] = (t < N) ? __fsub_rn(f.x, kb[2 * i]) : 0.0f;
+            kx[p][2 * i + 1] = (t < N) ? __fsub_rn(f.y, kb[2 * i + 1]) : 0.0f;
+            m = fmax3(m, fabsf(kx[p][2 * i]), fabsf(kx[p][2 * i + 1]));
+        }
 #pragma unroll
         for (int x = 1; x < 2 * TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
-        if (lane % (2 * TPR) == 0) atomicMax(&gmax[4 * (r / 64) + (r % 8) / 2], __float_as_uint(m));
+        gm[(p * RPP) / 64] = fmaxf(gm[(p * RPP) / 64], m);
+    }
+    constexpr int NSLOT = RPP / 8;
+    const int L = rofs / 2;
+    if (lane % (2 * TPR) == 0) {
+        gpart[L % 4][L / 4] = gm[0];
+        gpart[4 + L % 4][L / 4] = gm[1];
     }
     __syncthreads();
     // K codes (O-3) straight to the swizzled K^ tile image
     int8_t* kimg = khat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const int r = p * RPP + rofs, t = tile * kTile + r;
-        const float delta = __fdiv_rn(__uint_as_float(gmax[4 * (r / 64) + (r % 8) / 2]), (float)qk_max);
-        const float rd = __frcp_rn(delta);
-        const __half* kh = reinterpret_cast<const __half*>(&kraw[p]);
-        int code[8];
+        const int r = p * RPP + rofs;
+        const int g = 4 * (r / 64) + (r % 8) / 2;
+        float amax = gpart[g][0];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float kp = (t < N) ? __fsub_rn(__half2float(kh[i]), kbar[cg * 8 + i]) : 0.0f;
-            code[i] = quant_code_fast(kp, delta, rd, qk_max);
-        }
+        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[g][k]);
+        const float delta = __fdiv_rn(amax, (float)qk_max);
+        int code[8];
+        quant_codes8(kx[p], delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
-    if (threadIdx.x < 8)
-        dk[(size_t)bh * (nT * 8) + tile * 8 + threadIdx.x] =
-            __fdiv_rn(__uint_as_float(gmax[threadIdx.x]), (float)qk_max);
+    if (threadIdx.x < 8) {
+        float amax = gpart[threadIdx.x][0];
+#pragma unroll
+        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[threadIdx.x][k]);
+        dk[(size_t)bh * (nT * 8) + tile * 8 + threadIdx.x] = __fdiv_rn(amax, (float)qk_max);
+    }
     // V codes (O-4): thread = channel pair (c, c+1) x TOK consecutive tokens -> V^T rows c, c+1
     constexpr int NPAIR = D / 2, TOK = kTile / (256 / NPAIR);
     const int cp = threadIdx.x % NPAIR, t0 = (threadIdx.x / NPAIR) * TOK, c = 2 * cp;
     const float d0 = dvs[c], d1 = dvs[c + 1];
+    const float d0s = d0 != 0.0f ? d0 : 1.0f, d1s = d1 != 0.0f ? d1 : 1.0f;    // all-zero channel: codes 0
     const float m0 = vmean ? vmean[(size_t)bh * D + c] : 0.0f, m1 = vmean ? vmean[(size_t)bh * D + c + 1] : 0.0f;
     uint8_t* vimg = vhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
@@ -342,9 +386,11 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
                 const __half2 h = *reinterpret_cast<const __half2*>(&vt[(t0 + tb + 4 * q + e) * VS + c]);
                 const float2 f = __half22float2(h);
                 const bool pad = tile * kTile + t0 + tb + 4 * q + e >= N;   // padded token: code 0
+                const float q0 = __fdiv_rn(__fsub_rn(f.x, m0), d0s);         // V' = V - V_m
+                const float q1 = __fdiv_rn(__fsub_rn(f.y, m1), d1s);
                 float2 qv;
-                qv.x = (d0 != 0.0f && !pad) ? __fdiv_rn(__fsub_rn(f.x, m0), d0) : 0.0f;   // V' = V - V_m
-                qv.y = (d1 != 0.0f && !pad) ? __fdiv_rn(__fsub_rn(f.y, m1), d1) : 0.0f;
+                qv.x = (d0 != 0.0f && !pad) ? q0 : 0.0f;
+                qv.y = (d1 != 0.0f && !pad) ? q1 : 0.0f;
                 pr[e] = (uint32_t)__nv_cvt_float2_to_fp8x2(qv, __NV_SATFINITE, __NV_E4M3);   // lo = c, hi = c+1
             }
             const uint32_t x = pr[0] | (pr[1] << 16), y = pr[2] | (pr[3] << 16);
@@ -464,10 +510,8 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
 #pragma unroll
         for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[g][k]);
         const float delta = __fdiv_rn(amax, (float)qk_max);   // O-6
-        const float rd = __frcp_rn(delta);
         int code[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) code[i] = quant_code_fast(x[p][i], delta, rd, qk_max);
+        quant_codes8(x[p], delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
     if (threadIdx.x < 32) {
