@@ -115,10 +115,14 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
  * kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]), vmean(f32 [B*H_kv*d], smooth V V_m),
  * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][N_pad/4]), qbar(f32 [B*H_q][nT][d]),
  * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][N_pad/16]),
- * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), ds(f32 [B*H_q][nT][N_pad], scaled by
- * log2(e)/sqrt(d)), qbt(q_bar tf32 big/small split images [B*H_q][ceil(nT/256)][d/32][2][256*128 B],
- * input of the tensor-core Delta S GEMM), end) -- tile images are K-major, 128B (d=128) / 64B (d=64) swizzled, the exact
- * shared-memory image the tensor cores read.  Returns 0 or SAGE2_EINVAL. */
+ * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), qbt(q_bar tf32 big/small split images
+ * [B*H_q][ceil(nT/256)][d/32][2][256*128 B], input of the tensor-core Delta S GEMM), ds(f32, scaled
+ * by log2(e)/sqrt(d): [B*H_q][nT][N_pad] for non-causal calls; causal calls (SAGE2_F_CAUSAL given to
+ * sage2_prepare) store row i of a head with only its 128(i+1) visible keys, at 128*i*(i+1)/2 floats
+ * from the head's base 64*nT*(nT+1)*bhq -- half the bytes), end) -- the offsets returned here are
+ * the non-causal ones (identical except end).  Tile images are K-major, 128B (d=128) / 64B (d=64)
+ * swizzled, the exact shared-memory image the tensor cores read.
+ * Returns 0 or SAGE2_EINVAL. */
 #define SAGE2_WS_NREGIONS 15
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 

@@ -33,13 +33,22 @@ struct AttnParams {
     const uint8_t* vhat;    // [B*Hkv][nT] V^T tile images D x 128 (E4M3)
     const float* dv;        // [B*Hkv][D]
     const float* vmean;     // [B*Hkv][D] V_m of the optional smooth V, or null
-    const float* ds;        // [B*Hq][nT][N_pad]  Delta S * log2(e)/sqrt(d)
+    const float* ds;        // Delta S * log2(e)/sqrt(d): [B*Hq][nT][N_pad], or triangular (ds_tri)
+    int ds_tri;             // causal workspaces: row i of a head holds only keys < 128 (i + 1)
     __half* out;            // [B][Hq][N][D]
     int32_t* s_dump;        // debug: [B*Hq][N_pad][N_pad] raw S_int (DUMP builds only)
     uint8_t* p_dump;        // debug: [B*Hq][N_pad][N_pad] P^ codes (DUMP builds only; may be null)
     int Hq, Hkv, N, nT;
     float qk_scale_log2;    // log2(e)/sqrt(d)
 };
+
+// Offset of Delta S row (query block) i of head bhq: full [nT][N_pad] rows, or the causal compact
+// layout where row i keeps only the 128 (i + 1) keys a causal query block can see (NEXT#3).
+__host__ __device__ __forceinline__ size_t ds_row(int tri, int bhq, int i, int nT) {
+    const size_t Np = (size_t)nT * 128;
+    return tri ? (size_t)bhq * 64 * (size_t)nT * (nT + 1) + 64 * (size_t)i * (i + 1)
+               : ((size_t)bhq * nT + i) * Np;
+}
 
 constexpr int kStages = 3;
 constexpr float kLog2_448 = 8.807354922057604f;   // log2(448): folds the static P scale
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(192, 1) k_attn(const AttnParams p) {
                 mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 512 + 32);
                 bulk_g2s(sa, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s));
                 bulk_g2s(sa + L::TILE, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s));
-                bulk_g2s(sa + 2 * L::TILE, p.ds + ((size_t)bhq * nT + i) * Np + (size_t)j * 128, 512,
+                bulk_g2s(sa + 2 * L::TILE, p.ds + ds_row(p.ds_tri, bhq, i, nT) + (size_t)j * 128, 512,
                          bar_kv_full(s));
                 bulk_g2s(sa + 2 * L::TILE + 512, p.dk + (size_t)bhk * nT * 8 + (size_t)j * 8, 32, bar_kv_full(s));
             }

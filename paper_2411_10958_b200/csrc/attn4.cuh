@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(384, 1) k_attn4(const AttnParams p) {
                 mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 512 + 32);
                 bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
                 bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
-                bulk_g2s(sa + L::ST_DS, p.ds + ((size_t)bhq * nT + i) * Np + (size_t)j * 128, 512, bar_kv_full(s));
+                bulk_g2s(sa + L::ST_DS, p.ds + ds_row(p.ds_tri, bhq, i, nT) + (size_t)j * 128, 512, bar_kv_full(s));
                 bulk_g2s(sa + L::ST_DK, p.dk + (size_t)bhk * nT * 8 + (size_t)j * 8, 32, bar_kv_full(s));
             }
         } else if (warp == 1 && lane == 0) {

@@ -116,9 +116,9 @@ __global__ void __launch_bounds__(384, 1) k_attn6(const AttnParams p) {
                 bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
                 bulk_g2s(sa + L::ST_DK, p.dk + (size_t)bhk * nT * 8 + (size_t)j * 8, 32, bar_kv_full(s));
                 if (d0)
-                    bulk_g2s(sa + L::ST_DS0, p.ds + ((size_t)bhq * nT + it0) * Np + (size_t)j * 128, 512, bar_kv_full(s));
+                    bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
                 if (d1)
-                    bulk_g2s(sa + L::ST_DS1, p.ds + ((size_t)bhq * nT + it1) * Np + (size_t)j * 128, 512, bar_kv_full(s));
+                    bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, bhq, it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
             }
         } else if (warp == 9 || warp == 10) {
             // ===================== MMA issuer for Q tile k =====================

@@ -19,6 +19,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#include "attn.cuh"
 #include "prep.cuh"
 #include "ptx.cuh"
 
@@ -44,7 +45,10 @@ struct DsgSmem {
 template <int D>
 __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                        const uint8_t* __restrict__ qbt, int N, int Hq, int Hkv,
-                                                       int BHq, float scale_log2, float* __restrict__ ds) {
+                                                       int BHq, float scale_log2, float* __restrict__ ds, int tri) {
+    // tri (causal workspaces): only query blocks i >= kt see key tile kt; rows are stored in the
+    // compact triangular layout of ds_row() and items whose whole chunk lies above the diagonal are
+    // skipped by every role alike (the same `live` predicate).
     using L = DsgSmem<D>;
     constexpr int NA = L::NA;
     extern __shared__ uint8_t smem_raw[];
@@ -87,12 +91,18 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
         c = r % nch;
     };
     auto chunk_rows = [&](int c) { return min(kDsgChunk, nT - c * kDsgChunk); };
+    auto live = [&](int w) {
+        int bhq, kt, c;
+        decode(w, bhq, kt, c);
+        return !tri || c * kDsgChunk + chunk_rows(c) - 1 >= kt;
+    };
 
     if (warp < 4) {
         // ===================== A producers: K' = fp32(K - k_bar) -> tf32 big/small =====================
         const int t = threadIdx.x;
         uint32_t g = 0;
         for (int w = blockIdx.x; w < items; w += gridDim.x) {
+            if (!live(w)) continue;
             int bhq, kt, c;
             decode(w, bhq, kt, c);
             const int b = bhq / Hq, hk = (bhq % Hq) / (Hq / Hkv), bhk = b * Hkv + hk;
@@ -134,21 +144,30 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
         const int t = threadIdx.x - 128;
         const uint32_t lane_off = (uint32_t)(32 * (warp - 4)) << 16;
         uint32_t m = 0;
-        for (int w = blockIdx.x; w < items; w += gridDim.x, ++m) {
+        for (int w = blockIdx.x; w < items; w += gridDim.x) {
+            if (!live(w)) continue;
             int bhq, kt, c;
             decode(w, bhq, kt, c);
             const int buf = m & 1, ni = chunk_rows(c);
             mbar_wait(acc_full(buf), (m >> 1) & 1);
+            ++m;
             tc_fence_after();
-            float* out = ds + ((size_t)bhq * nT + (size_t)c * kDsgChunk) * Np + (size_t)kt * 128 + t;
+            const int i0 = c * kDsgChunk;
+            // row pointer advanced incrementally (row i -> i+1: N_pad floats, or 128 (i+1) in the
+            // triangular layout): the epilogue warps are the throughput limit of this kernel
+            float* rp = ds + ds_row(tri, bhq, i0, nT) + (size_t)kt * 128 + t;
+            size_t stride = tri ? (size_t)128 * (i0 + 1) : (size_t)Np;
             for (int col0 = 0; col0 < ni; col0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem + buf * 256 + col0 + lane_off, r);
                 tmem_wait_ld();
                 reg_dep32(r);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (col0 + j < ni) __stcs(out + (size_t)(col0 + j) * Np, __uint_as_float(r[j]) * scale_log2);
+                for (int j = 0; j < 32; ++j) {
+                    if (col0 + j < ni && (!tri || i0 + col0 + j >= kt)) __stcs(rp, __uint_as_float(r[j]) * scale_log2);
+                    rp += stride;
+                    if (tri) stride += 128;
+                }
             }
             tc_fence_before();
             mbar_arrive(acc_empty(buf));
@@ -157,13 +176,15 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
         if (lane == 0) {
             // ===================== MMA issuer =====================
             uint32_t g = 0, m = 0;
-            for (int w = blockIdx.x; w < items; w += gridDim.x, ++m) {
+            for (int w = blockIdx.x; w < items; w += gridDim.x) {
+                if (!live(w)) continue;
                 int bhq, kt, c;
                 decode(w, bhq, kt, c);
                 const int ni = chunk_rows(c), nmma = (ni + 15) & ~15;
                 const uint32_t idesc = idesc_tf32(128, nmma);
                 const int buf = m & 1;
                 if (m >= 2) mbar_wait(acc_empty(buf), ((m >> 1) - 1) & 1);
+                ++m;
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 for (int a = 0; a < NA; ++a, ++g) {
@@ -190,6 +211,7 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
             // ===================== B loader (pre-split q_bar slices) =====================
             uint32_t g = 0;
             for (int w = blockIdx.x; w < items; w += gridDim.x) {
+                if (!live(w)) continue;
                 int bhq, kt, c;
                 decode(w, bhq, kt, c);
                 const int nmma = (chunk_rows(c) + 15) & ~15;

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
 template <int D>
 __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                  const float* __restrict__ qbar, int N, int Hq, int Hkv,
-                                                 float scale_log2, float* __restrict__ ds) {
+                                                 float scale_log2, float* __restrict__ ds, int tri) {
     constexpr int ICH = 32;                            // Q blocks per smem chunk
     const int kt = blockIdx.x, bhq = blockIdx.y, nT = gridDim.x, Np = nT * kTile;
     const int b = bhq / Hq, hq = bhq % Hq, hk = hq / (Hq / Hkv);
@@ -552,8 +552,11 @@ __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, c
         for (int c = 0; c < D; ++c) kp[c] = 0.0f;
     }
     const float* qb = qbar + (size_t)bhq * nT * D;
-    float* out = ds + (size_t)bhq * nT * Np;
-    for (int i0 = 0; i0 < nT; i0 += ICH) {
+    // row offsets as ds_row() (attn.cuh): full rows, or the causal triangular layout (i >= kt only)
+    auto row = [&](int i) {
+        return tri ? (size_t)bhq * 64 * (size_t)nT * (nT + 1) + 64 * (size_t)i * (i + 1) : ((size_t)bhq * nT + i) * Np;
+    };
+    for (int i0 = tri ? (kt / ICH) * ICH : 0; i0 < nT; i0 += ICH) {
         const int ni = min(ICH, nT - i0);
         __syncthreads();
         for (int e = threadIdx.x; e < ni * D; e += 128) sq[e / D][e % D] = qb[(size_t)i0 * D + e];
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, c
             float acc = 0.0f;
 #pragma unroll
             for (int c = 0; c < D; ++c) acc = fmaf(sq[ii][c], kp[c], acc);
-            out[(size_t)(i0 + ii) * Np + t] = acc * scale_log2;
+            if (!tri || i0 + ii >= kt) ds[row(i0 + ii) + t] = acc * scale_log2;
         }
     }
 }

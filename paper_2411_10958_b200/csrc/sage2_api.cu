@@ -62,7 +62,7 @@ struct Layout {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
+Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
     const size_t nT = (size_t)(N + 127) / 128, Np = nT * 128;
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
     const size_t sizes[SAGE2_WS_NREGIONS - 1] = {
@@ -78,8 +78,10 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
         BHk * Np * d,         // khat
         BHk * (Np / 16) * 4,  // dk
         BHk * Np * d,         // vhat
-        BHq * nT * Np * 4,    // ds
         BHq * ((nT + 255) / 256) * (size_t)(d / 32) * 65536,   // qbt (q_bar tf32 split images)
+        // ds last (its size is the only one that depends on causal): full [nT][N_pad] rows, or the
+        // triangular causal layout of ds_row() (attn.cuh), half the bytes
+        causal ? BHq * 64 * nT * (nT + 1) * 4 : BHq * nT * Np * 4,
     };
     Layout L;
     size_t o = 0;
@@ -91,7 +93,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d) {
     return L;
 }
 
-enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_DS, R_QBT, R_END };
+enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_QBT, R_DS, R_END };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -108,6 +110,7 @@ template <int D>
 int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int Hq, int Hkv, int N, int flags,
                    uint8_t* ws, const Layout& L, cudaStream_t st) {
     const int nT = (N + 127) / 128;
+    const bool causal = (flags & SAGE2_F_CAUSAL) != 0;     // Delta S in the triangular layout
     const int qk_max = (flags & SAGE2_F_INT8) ? 127 : 7;
     const int smooth_q = (flags & SAGE2_F_INT8) ? 0 : 1;   // SageAttn2-8b: no Q smoothing
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
@@ -136,7 +139,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     if (flags & SAGE2_F_DS_SIMT) {
         k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                     reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
-                                                    scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]));
+                                                    scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
         return cuda_rc();
     }
     static bool configured = false;
@@ -154,7 +157,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const int grid = (int)std::min<long long>(items, nsm);
     k_delta_s_tc<D><<<grid, 320, DsgSmem<D>::ALLOC, st>>>(
         k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]), ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2,
-        reinterpret_cast<float*>(ws + L.off[R_DS]));
+        reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
     return cuda_rc();
 }
 
@@ -263,6 +266,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.dv = reinterpret_cast<const float*>(ws + L.off[R_DV]);
     p.vmean = (flags & SAGE2_F_SMOOTH_V) ? reinterpret_cast<const float*>(ws + L.off[R_VMEAN]) : nullptr;
     p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
+    p.ds_tri = (flags & SAGE2_F_CAUSAL) ? 1 : 0;
     p.out = reinterpret_cast<__half*>(out);
     p.s_dump = s_dump;
     p.p_dump = p_dump;
@@ -405,9 +409,9 @@ const char* sage2_strerror(int code) {
     }
 }
 
-size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int /*causal*/) {
+size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int causal) {
     if (!shapes_ok(B, H_q, H_kv, N, d)) return 0;
-    return make_layout(B, H_q, H_kv, N, d).off[R_END];
+    return make_layout(B, H_q, H_kv, N, d, causal != 0).off[R_END];
 }
 
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets) {
@@ -423,7 +427,7 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q || !k || !v || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (reinterpret_cast<uintptr_t>(workspace) & 255)) return SAGE2_EINVAL;
-    Layout L = make_layout(B, H_q, H_kv, N, d);
+    Layout L = make_layout(B, H_q, H_kv, N, d, (flags & SAGE2_F_CAUSAL) != 0);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     auto* ws = reinterpret_cast<uint8_t*>(workspace);
@@ -439,7 +443,7 @@ int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out) || !flags_ok(flags)) return SAGE2_EINVAL;
-    Layout L = make_layout(B, H_q, H_kv, N, d);
+    Layout L = make_layout(B, H_q, H_kv, N, d, (flags & SAGE2_F_CAUSAL) != 0);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     return launch_attention(out, nullptr, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
                             reinterpret_cast<cudaStream_t>(stream));

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("SAGE2_LIB") or os.path.join(_HERE, "libsage2.so")
 F_CAUSAL = 1
 F_INT8 = 2
 WS_NREGIONS = 15
-REGIONS = ("ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "ds", "qbt", "end")
+REGIONS = ("ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "qbt", "ds", "end")
 
 _lib = None
 
@@ -94,8 +94,10 @@ def flags(causal=False, int8=False, qk_e4m3=False, smooth_v=False):
             (F_SMOOTH_V if smooth_v else 0))
 
 
-def workspace_bytes(B, Hq, Hkv, N, d):
-    return int(lib().sage2_workspace_bytes(B, Hq, Hkv, N, d, 0))
+def workspace_bytes(B, Hq, Hkv, N, d, causal=False):
+    """Workspace size; causal=True sizes Delta S in the triangular causal layout (half the bytes) --
+    such a workspace only serves causal prepare/attention calls.  The non-causal size serves both."""
+    return int(lib().sage2_workspace_bytes(B, Hq, Hkv, N, d, int(causal)))
 
 
 def layout(B, Hq, Hkv, N, d):
@@ -104,8 +106,8 @@ def layout(B, Hq, Hkv, N, d):
     return dict(zip(REGIONS, [int(o) for o in offs]))
 
 
-def alloc_workspace(B, Hq, Hkv, N, d, device="cuda"):
-    return torch.empty(workspace_bytes(B, Hq, Hkv, N, d), dtype=torch.uint8, device=device)
+def alloc_workspace(B, Hq, Hkv, N, d, device="cuda", causal=False):
+    return torch.empty(workspace_bytes(B, Hq, Hkv, N, d, causal), dtype=torch.uint8, device=device)
 
 
 def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=False, smooth_v=False):

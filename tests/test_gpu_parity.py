@@ -319,3 +319,30 @@ def test_smooth_v_output_parity(B, Hq, Hkv, N, d, causal):
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
                                    OracleConfig(causal=causal, smooth_v=True), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
+
+
+@pytest.mark.parametrize("N,d", [(300, 64), (1000, 128)])
+def test_causal_compact_delta_s(N, d):
+    """NEXT#3: causal preprocessing stores Delta S in the triangular layout (row i keeps keys
+    < 128 (i+1)); every stored value equals the full-layout value bit for bit, and the causal
+    workspace is about half the size."""
+    B, Hq, Hkv = 1, 2, 1
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=17)
+    wf = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    wc = sage2.alloc_workspace(B, Hq, Hkv, N, d, causal=True)
+    sage2.prepare(qg, kg, vg, wf)
+    sage2.prepare(qg, kg, vg, wc, causal=True)
+    torch.cuda.synchronize()
+    lay = sage2.layout(B, Hq, Hkv, N, d)
+    nT = (N + 127) // 128
+    Np = nT * 128
+    full = wf[lay["ds"]:lay["ds"] + B * Hq * nT * Np * 4].cpu().numpy().view(np.float32).reshape(B * Hq, nT, Np)
+    ntri = B * Hq * 64 * nT * (nT + 1)
+    tri = wc[lay["ds"]:lay["ds"] + ntri * 4].cpu().numpy().view(np.float32)
+    for bh in range(B * Hq):
+        for i in range(nT):
+            off = bh * 64 * nT * (nT + 1) + 64 * i * (i + 1)
+            got = tri[off:off + 128 * (i + 1)]
+            assert np.array_equal(got.view(np.uint32), full[bh, i, :128 * (i + 1)].view(np.uint32))
+    # config C4 (Llama-3.1-8B-like, N = 100000 causal): 10.7 GB -> 5.7 GB of workspace
+    assert sage2.workspace_bytes(1, 32, 8, 100000, 128, causal=True) < 0.55 * sage2.workspace_bytes(1, 32, 8, 100000, 128)
