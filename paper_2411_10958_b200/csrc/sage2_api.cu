@@ -496,30 +496,72 @@ int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, in
 
 int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, void* out_host, int B, int H_q,
                     int H_kv, int N, int d, int causal, void* stream) {
+    // Pipelined over chunks of (b, h_kv) units (one KV head + its H_q/H_kv query heads; contiguous
+    // in every [B, H, N, d] tensor and independent): chunk c runs H2D ->
+    // prepare -> attention -> D2H on internal stream c % 2, so the copy engines of one chunk overlap
+    // the kernels of the other.  Two device buffer sets (inputs, output, workspace) are reused.
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q_host || !k_host || !v_host || !out_host) return SAGE2_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const size_t qb = (size_t)B * H_q * N * d * 2, kb = (size_t)B * H_kv * N * d * 2;
-    const size_t wsb = sage2_workspace_bytes(B, H_q, H_kv, N, d, causal);
-    void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *ws = nullptr;
-    if (cudaMallocAsync(&dq, qb, st) != cudaSuccess || cudaMallocAsync(&dk, kb, st) != cudaSuccess ||
-        cudaMallocAsync(&dv, kb, st) != cudaSuccess || cudaMallocAsync(&dout, qb, st) != cudaSuccess ||
-        cudaMallocAsync(&ws, wsb, st) != cudaSuccess) {
-        cudaGetLastError();
-        rc = SAGE2_ENOMEM;
+    const int grp = H_q / H_kv, units = B * H_kv;
+    int nch = units < 8 ? units : 8;
+    const int U = (units + nch - 1) / nch;                 // units per chunk
+    nch = (units + U - 1) / U;
+    const size_t qu = (size_t)grp * N * d * 2, ku = (size_t)N * d * 2;   // bytes per unit
+    const size_t wsb = sage2_workspace_bytes(1, U * grp, U, N, d, causal);
+    const int nbuf = nch < 2 ? nch : 2;
+    void* buf[2][5] = {{nullptr}};
+    cudaStream_t ss[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_done[2] = {nullptr, nullptr};
+    auto bad = [&]() { if (rc == SAGE2_OK) rc = cuda_rc(); };
+    for (int i = 0; i < nbuf && rc == SAGE2_OK; ++i) {
+        if (cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming) != cudaSuccess)
+            bad();
+        const size_t sz[5] = {U * qu, U * ku, U * ku, U * qu, wsb};
+        for (int r = 0; r < 5 && rc == SAGE2_OK; ++r)
+            if (cudaMallocAsync(&buf[i][r], sz[r], st) != cudaSuccess) {
+                cudaGetLastError();
+                rc = SAGE2_ENOMEM;
+            }
     }
-    if (rc == SAGE2_OK) {
-        if (cudaMemcpyAsync(dq, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            cudaMemcpyAsync(dk, k_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            cudaMemcpyAsync(dv, v_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess)
-            rc = cuda_rc();
+    if (rc == SAGE2_OK && (cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) != cudaSuccess ||
+                           cudaEventRecord(ev_start, st) != cudaSuccess))
+        bad();
+    for (int i = 0; i < nbuf && rc == SAGE2_OK; ++i)
+        if (cudaStreamWaitEvent(ss[i], ev_start, 0) != cudaSuccess) bad();   // allocations are ready
+    const int flags = causal ? SAGE2_F_CAUSAL : 0;
+    for (int c = 0; c < nch && rc == SAGE2_OK; ++c) {
+        const int i = c % 2, u0 = c * U, nu = (units - u0) < U ? (units - u0) : U;
+        cudaStream_t s = ss[i];
+        const char* qh = static_cast<const char*>(q_host) + (size_t)u0 * qu;
+        const char* kh = static_cast<const char*>(k_host) + (size_t)u0 * ku;
+        const char* vh = static_cast<const char*>(v_host) + (size_t)u0 * ku;
+        char* oh = static_cast<char*>(out_host) + (size_t)u0 * qu;
+        if (cudaMemcpyAsync(buf[i][0], qh, nu * qu, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(buf[i][1], kh, nu * ku, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(buf[i][2], vh, nu * ku, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            bad();
+            break;
+        }
+        rc = sage2_attn_ex(buf[i][0], buf[i][1], buf[i][2], buf[i][3], 1, nu * grp, nu, N, d, flags, buf[i][4],
+                           wsb, s);
+        if (rc == SAGE2_OK && cudaMemcpyAsync(oh, buf[i][3], nu * qu, cudaMemcpyDeviceToHost, s) != cudaSuccess) bad();
     }
-    if (rc == SAGE2_OK) rc = sage2_attn_ws(dq, dk, dv, dout, B, H_q, H_kv, N, d, causal, ws, wsb, stream);
-    if (rc == SAGE2_OK && cudaMemcpyAsync(out_host, dout, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        rc = cuda_rc();
-    for (void* p : {dq, dk, dv, dout, ws})
-        if (p) cudaFreeAsync(p, st);
+    for (int i = 0; i < nbuf; ++i) {
+        if (ss[i] && ev_done[i]) {
+            cudaEventRecord(ev_done[i], ss[i]);
+            cudaStreamWaitEvent(st, ev_done[i], 0);        // the caller's stream sees every chunk done
+        }
+        for (int r = 0; r < 5; ++r)
+            if (buf[i][r]) cudaFreeAsync(buf[i][r], st);
+    }
+    for (int i = 0; i < nbuf; ++i) {
+        if (ev_done[i]) cudaEventDestroy(ev_done[i]);
+        if (ss[i]) cudaStreamDestroy(ss[i]);               // released once its work completes
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
     return rc;
 }
 

@@ -196,6 +196,19 @@ def test_deterministic():
     assert torch.equal(o1, o2)
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(2, 8, 4, 300, 64, True), (3, 12, 3, 513, 128, False),
+                                                 (1, 20, 20, 256, 128, True)])
+def test_host_entry_point_pipelined_chunks(B, Hq, Hkv, N, d, causal):
+    """sage2_attn_host splits the (b, h_kv) units into up to 8 chunks on two streams (ragged last
+    chunk for 9 and 20 units); the result is bitwise the one-shot device result."""
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=8)
+    od = sage2.attn(qg, kg, vg, causal=causal)
+    oh = torch.empty_like(q).pin_memory()
+    sage2.attn_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), oh, causal=causal)
+    torch.cuda.synchronize()
+    assert torch.equal(od.cpu(), oh)
+
+
 def test_host_entry_point_matches_device():
     q, k, v, qg, kg, vg = _inputs(1, 2, 1, 500, 64, "structured", seed=6)
     od = sage2.attn(qg, kg, vg, causal=True)
