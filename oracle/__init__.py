@@ -19,6 +19,9 @@ from .oracle import (  # noqa: F401
     fp22_truncate,
     group_q,
     group_k,
+    group_q_g,
+    group_k_g,
+    ngroups,
     kv_head,
     q_block,
     delta_s,

@@ -32,7 +32,7 @@ def build(force=False):
 class _Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "b_q", "kv_tile", "causal", "quant", "qk_max", "smooth_q", "smooth_k",
-        "pv_mode", "two_level", "smooth_v", "p_fp32")] + [("amb_eta", ctypes.c_double)]
+        "pv_mode", "two_level", "smooth_v", "p_fp32", "qk_gran")] + [("amb_eta", ctypes.c_double)]
 
 
 @dataclass
@@ -49,12 +49,13 @@ class OracleConfig:
     two_level: bool = True
     smooth_v: bool = False
     p_fp32: bool = True       # P^ decision in the kernel's precision (C-21)
+    qk_gran: int = 0          # 0 per-thread (SageAttn2), 1 per-block, 2 per-token (NEXT#4 ablation)
     amb_eta: float = 2.0 ** -12
 
     def c(self):
         return _Cfg(self.b_q, self.kv_tile, int(self.causal), int(self.quant), self.qk_max,
                     int(self.smooth_q), int(self.smooth_k), self.pv_mode, int(self.two_level),
-                    int(self.smooth_v), int(self.p_fp32), float(self.amb_eta))
+                    int(self.smooth_v), int(self.p_fp32), int(self.qk_gran), float(self.amb_eta))
 
 
 def lib():
@@ -73,6 +74,10 @@ def lib():
             L.orc_e4m3_decode.argtypes = [ctypes.c_uint8]
             L.orc_group_q.argtypes = [I]
             L.orc_group_k.argtypes = [I]
+            L.orc_group_q_g.argtypes = [I, I]
+            L.orc_group_k_g.argtypes = [I, I]
+            L.orc_ngroups_q.argtypes = [I]
+            L.orc_ngroups_k128.argtypes = [I]
             for n in ("orc_e4m3_encode_array", "orc_e4m3_decode_array", "orc_fp16_decode_array",
                       "orc_fp16_round_array", "orc_fp22_truncate_array"):
                 getattr(L, n).argtypes = [P, ctypes.c_long, P]
@@ -145,6 +150,19 @@ def group_k(t):
     return lib().orc_group_k(int(t))
 
 
+def group_q_g(t, gran):
+    return lib().orc_group_q_g(int(t), int(gran))
+
+
+def group_k_g(t, gran):
+    return lib().orc_group_k_g(int(t), int(gran))
+
+
+def ngroups(gran):
+    """(Q groups per 128-token block, K groups per 128 keys) of a granularity."""
+    return lib().orc_ngroups_q(int(gran)), lib().orc_ngroups_k128(int(gran))
+
+
 def _bits(x):
     x = np.ascontiguousarray(x)
     if x.dtype == np.float16:
@@ -160,7 +178,7 @@ def kv_head(K, V, cfg=OracleConfig()):
     N, d = K.shape
     Np = (N + 127) // 128 * 128
     r = dict(kbar=np.zeros(d, np.float32), kprime=np.zeros((N, d), np.float32),
-             khat=np.zeros((Np, d), np.int8), dk=np.zeros(Np // 16, np.float32),
+             khat=np.zeros((Np, d), np.int8), dk=np.zeros(Np // 128 * ngroups(cfg.qk_gran)[1], np.float32),
              vhat=np.zeros((Np, d), np.uint8), dv=np.zeros(d, np.float32),
              vmean=np.zeros(d, np.float32))
     c = cfg.c()
@@ -170,11 +188,12 @@ def kv_head(K, V, cfg=OracleConfig()):
 
 
 def q_block(Qblk, cfg=OracleConfig()):
-    """One Q block (rows present, <= 128, fp16).  Returns dict qbar, qhat[128,d], dq[32]."""
+    """One Q block (rows present, <= 128, fp16).  Returns dict qbar, qhat[128,d], dq[groups]
+    (32 per-thread groups by default)."""
     Qb = _bits(Qblk)
     n, d = Qb.shape
     r = dict(qbar=np.zeros(d, np.float32), qhat=np.zeros((128, d), np.int8),
-             dq=np.zeros(32, np.float32))
+             dq=np.zeros(ngroups(cfg.qk_gran)[0], np.float32))
     c = cfg.c()
     lib().orc_q_block(_p(Qb), n, d, ctypes.byref(c), _p(r["qbar"]), _p(r["qhat"]), _p(r["dq"]))
     return r

@@ -50,6 +50,9 @@ typedef struct {
     int p_fp32;     /* 1: the P^ code decision is taken in the kernel's precision (fp32 scores in
                        base 2, P~*448 rounded to fp32 before the E4M3 cast) -- DESIGN.md C-21;
                        0: everything in fp64 (the paper's formulas verbatim)                    */
+    int qk_gran;    /* Q/K quantization granularity (NEXT#4 ablation):
+                       0 per-thread (SageAttn2), 1 per-block (Q: 128-token block, K: 64-token
+                       block), 2 per-token (every token its own group)                   */
     double amb_eta; /* relative distance to an E4M3 rounding midpoint under which a P^ decision is
                        reported "ambiguous" (the fp32 precision gap, C-21)             */
 } orc_cfg;
@@ -149,6 +152,14 @@ int orc_group_q(int t) { return 8 * (t / 32) + (t % 8); }
  * scale"; 4 groups per 64-token block. */
 int orc_group_k(int t) { return 4 * (t / 64) + (t % 8) / 2; }
 
+/* Granularity-general group maps (NEXT#4).  Q: token t of a 128-token block -> group in the block;
+ * K: key token t -> group in the head.  Per-block groups follow SageAttention's blocks (b_q = 128,
+ * b_k = 64); per-token groups are single tokens. */
+int orc_ngroups_q(int gran) { return gran == 1 ? 1 : gran == 2 ? 128 : 32; }
+int orc_ngroups_k128(int gran) { return gran == 1 ? 2 : gran == 2 ? 128 : 8; }   /* per 128 keys */
+int orc_group_q_g(int t, int gran) { return gran == 1 ? 0 : gran == 2 ? t : orc_group_q(t); }
+int orc_group_k_g(int t, int gran) { return gran == 1 ? t / 64 : gran == 2 ? t : orc_group_k(t); }
+
 /* ------------------------------------------------------------------------------------------ */
 /* Quantizer psi: delta = max|A|/qmax, A_hat = round(A/delta), clamp.              */
 /* ------------------------------------------------------------------------------------------ */
@@ -188,7 +199,8 @@ static double exact_mean_f64(const uint16_t* X, int d, int r0, int r1, int c) {
  *   kbar[d]          fp32 k_bar (O-1)            (zero if !smooth_k)
  *   kprime[N*d]      fp32 gamma(K) = K - k_bar  (O-2)
  *   khat[N_pad*d]    int8 codes (O-3)
- *   dk[N_pad/16]     fp32 delta_K per group g_K  (O-3; groups with no token: 0)
+ *   dk[N_pad/128 * orc_ngroups_k128]  fp32 delta_K per group g_K (O-3; N_pad/16 per-thread
+ *                    groups by default; groups with no token: 0)
  *   vhat[N_pad*d]    E4M3 codes (O-4)
  *   dv[d]            fp32 delta_V per channel   (O-4, reading C-15)
  *   vmean[d]         fp32 V_m (smooth_v only; else zero)
@@ -204,21 +216,21 @@ int orc_kv_head(const uint16_t* K, const uint16_t* V, int N, int d, const orc_cf
         for (int c = 0; c < d; ++c)
             kprime[(size_t)t * d + c] = f32_sub((float)orc_fp16_decode(K[(size_t)t * d + c]), kbar[c]);
     /* O-3: per-thread groups g_K, delta_K = max|K'|/qmax, codes */
-    int ng = Np / 16;
-    for (int g = 0; g < ng; ++g) dk[g] = 0.0f;
-    float* amax = (float*)calloc((size_t)ng, sizeof(float));
+    size_t ng = (size_t)(Np / 128) * (size_t)orc_ngroups_k128(cfg->qk_gran);
+    for (size_t g = 0; g < ng; ++g) dk[g] = 0.0f;
+    float* amax = (float*)calloc(ng, sizeof(float));
     for (int t = 0; t < N; ++t) {
-        int g = orc_group_k(t);
+        int g = orc_group_k_g(t, cfg->qk_gran);
         for (int c = 0; c < d; ++c) {
             float a = fabsf(kprime[(size_t)t * d + c]);
             if (a > amax[g]) amax[g] = a;
         }
     }
-    for (int g = 0; g < ng; ++g) dk[g] = f32_div(amax[g], (float)cfg->qk_max);
+    for (size_t g = 0; g < ng; ++g) dk[g] = f32_div(amax[g], (float)cfg->qk_max);
     free(amax);
     memset(khat, 0, (size_t)Np * d);
     for (int t = 0; t < N; ++t) {
-        float delta = dk[orc_group_k(t)];
+        float delta = dk[orc_group_k_g(t, cfg->qk_gran)];
         for (int c = 0; c < d; ++c)
             khat[(size_t)t * d + c] = (int8_t)quant_code(kprime[(size_t)t * d + c], delta, cfg->qk_max);
     }
@@ -246,25 +258,27 @@ int orc_kv_head(const uint16_t* K, const uint16_t* V, int N, int d, const orc_cf
 /* Preprocessing of one Q block i:  Alg. 1 "q_bar_i = mean(Q_i), (dQ, Q^_i) = psi_Q(Q_i - q_bar_i)" */
 /* ------------------------------------------------------------------------------------------ */
 /* Qblk: rows [0, n) of the block (n = present tokens, <= 128), fp16 bits, row stride d.
- * Outputs: qbar[d] fp32 (O-5), qhat[128*d] int8 (rows >= n zero), dq[32] fp32 (O-6). */
+ * Outputs: qbar[d] fp32 (O-5), qhat[128*d] int8 (rows >= n zero), dq[orc_ngroups_q] fp32 (O-6;
+ * 32 per-thread groups by default). */
 int orc_q_block(const uint16_t* Qblk, int n, int d, const orc_cfg* cfg,
                 float* qbar, int8_t* qhat, float* dq) {
     for (int c = 0; c < d; ++c) qbar[c] = cfg->smooth_q ? exact_mean_f32(Qblk, d, 0, n, c) : 0.0f;
-    float amax[32];
-    for (int g = 0; g < 32; ++g) amax[g] = 0.0f;
+    const int ngq = orc_ngroups_q(cfg->qk_gran);
+    float amax[128];
+    for (int g = 0; g < ngq; ++g) amax[g] = 0.0f;
     float* qp = (float*)malloc(sizeof(float) * (size_t)n * d);
     for (int t = 0; t < n; ++t)
         for (int c = 0; c < d; ++c) {
             float x = f32_sub((float)orc_fp16_decode(Qblk[(size_t)t * d + c]), qbar[c]);
             qp[(size_t)t * d + c] = x;
             float a = fabsf(x);
-            int g = orc_group_q(t);
+            int g = orc_group_q_g(t, cfg->qk_gran);
             if (a > amax[g]) amax[g] = a;
         }
-    for (int g = 0; g < 32; ++g) dq[g] = f32_div(amax[g], (float)cfg->qk_max);
+    for (int g = 0; g < ngq; ++g) dq[g] = f32_div(amax[g], (float)cfg->qk_max);
     memset(qhat, 0, (size_t)128 * d);
     for (int t = 0; t < n; ++t) {
-        float delta = dq[orc_group_q(t)];
+        float delta = dq[orc_group_q_g(t, cfg->qk_gran)];
         for (int c = 0; c < d; ++c)
             qhat[(size_t)t * d + c] = (int8_t)quant_code(qp[(size_t)t * d + c], delta, cfg->qk_max);
     }
@@ -365,7 +379,8 @@ int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
                     int64_t si = 0;
                     for (int c = 0; c < d; ++c)
                         si += (int64_t)qhat[(size_t)rr * d + c] * (int64_t)khat[(size_t)t * d + c];
-                    s = ((double)si * (double)dq[orc_group_q(rr)] * (double)dk[orc_group_k(t)] + ds[t]) * inv_sqrt_d;
+                    s = ((double)si * (double)dq[orc_group_q_g(rr, cfg->qk_gran)] *
+                             (double)dk[orc_group_k_g(t, cfg->qk_gran)] + ds[t]) * inv_sqrt_d;
                     if (cfg->p_fp32) s = (double)(float)(s * LOG2E);
                 }
                 S[t - j0] = s;

@@ -44,6 +44,25 @@ def _kgroups(n_tokens, n_pad):
     return groups
 
 
+def _qgroups_g(n_tokens, gran):
+    """Q groups of a 128-token block for a granularity (NEXT#4): 0 per-thread, 1 the
+    whole block, 2 one token each."""
+    if gran == 1:
+        return [list(range(n_tokens))]
+    if gran == 2:
+        return [[t] if t < n_tokens else [] for t in range(128)]
+    return _qgroups(n_tokens)
+
+
+def _kgroups_g(n_tokens, n_pad, gran):
+    """K groups for a granularity: 0 per-thread, 1 64-token blocks, 2 tokens."""
+    if gran == 1:
+        return [[t for t in range(b, b + 64) if t < n_tokens] for b in range(0, n_pad, 64)]
+    if gran == 2:
+        return [[t] if t < n_tokens else [] for t in range(n_pad)]
+    return _kgroups(n_tokens, n_pad)
+
+
 def _quant_groups(X, groups, qmax, n_rows):
     codes = np.zeros((n_rows, X.shape[1]), np.int64)
     deltas = []
@@ -62,7 +81,7 @@ def _quant_groups(X, groups, qmax, n_rows):
     return codes, deltas
 
 
-def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True):
+def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True, gran=0):
     """Q, K, V: [N, d] float16 numpy (one head).  Returns O [N, d] fp64 before fp16 rounding.
 
     p_fp32: scores held as fp32 in base 2 (S log2 e) and 448 P~ rounded to fp32 before the
@@ -72,7 +91,7 @@ def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True):
     Kf = K.astype(np.float32)
     kbar = np.array([_mean_f32(K[:, c].astype(np.float64)) for c in range(d)], np.float32)
     Kp = (Kf - kbar).astype(np.float32)                       # gamma(K) = K - mean(K)
-    kgroups = _kgroups(N, n_pad)
+    kgroups = _kgroups_g(N, n_pad, gran)
     khat, dks = _quant_groups(Kp, kgroups, qmax, N)
     dk_of = {}
     for gi, toks in enumerate(kgroups):
@@ -90,9 +109,9 @@ def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True):
         Qb = Q[rows]
         qbar = np.array([_mean_f32(Qb[:, c].astype(np.float64)) for c in range(d)], np.float32)
         Qp = (Qb.astype(np.float32) - qbar).astype(np.float32)
-        qhat, dqs = _quant_groups(Qp, _qgroups(len(rows)), qmax, len(rows))
+        qhat, dqs = _quant_groups(Qp, _qgroups_g(len(rows), gran), qmax, len(rows))
         dq_of = {}
-        for gi, toks in enumerate(_qgroups(len(rows))):
+        for gi, toks in enumerate(_qgroups_g(len(rows), gran)):
             for t in toks:
                 dq_of[t] = dqs[gi]
         dS = [sum(float(qbar[c]) * float(Kp[t, c]) for c in range(d)) for t in range(N)]

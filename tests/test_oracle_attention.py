@@ -213,3 +213,31 @@ def test_smooth_v_helps_channel_biased_v(orc):
         O = _oracle_head(orc, Q, K, V, OracleConfig(smooth_v=sv))
         err[sv] = orc.rmse(ref, O)
     assert err[True] < err[False]
+
+
+@pytest.mark.parametrize("gran", [1, 2])
+@pytest.mark.parametrize("N,kv_tile,causal", [(16, 4, True), (13, 128, False)])
+def test_granularity_vs_naive(orc, gran, N, kv_tile, causal):
+    """NEXT#4 ablation granularities (1 per-block, 2 per-token) against the naive implementation,
+    whose group lists are written out independently (tests/_naive.py)."""
+    d = 64
+    Q, K, V = rnd((N, d), 29, 1, 2), rnd((N, d), 30, 1, -1), rnd((N, d), 31)
+    ref = sage2_naive(Q, K, V, causal=causal, kv_tile=kv_tile, gran=gran)
+    got = _oracle_head(orc, Q, K, V, OracleConfig(kv_tile=kv_tile, causal=causal, qk_gran=gran))
+    assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_granularity_accuracy_ordering(orc):
+    """Direction of the paper's granularity ablation: finer groups are more accurate --
+    per-token >= per-thread > per-block on channel-outlier data (INT4)."""
+    N, d = 512, 64
+    g = np.random.default_rng(71)
+    mu = g.uniform(-2, 2, d)
+    mu[[5, 30]] = [15, -15]
+    scale = np.exp(g.normal(0, 1.0, (N, 1)))               # token-wise magnitude spread
+    Q = ((g.standard_normal((N, d)) + mu) * scale).astype(np.float16)
+    K = ((g.standard_normal((N, d)) + mu) * scale[::-1]).astype(np.float16)
+    V = g.standard_normal((N, d)).astype(np.float16)
+    ref = dense_attention(Q, K, V, False)
+    err = {gr: orc.rmse(ref, _oracle_head(orc, Q, K, V, OracleConfig(qk_gran=gr))) for gr in (0, 1, 2)}
+    assert err[2] <= err[0] < err[1], err

@@ -175,3 +175,24 @@ def test_code_range(orc, qk_max):
     X = (g.standard_normal((128, 64)) * 10).astype(np.float16)
     r = orc.q_block(X, OracleConfig(qk_max=qk_max))
     assert np.max(np.abs(r["qhat"].astype(int))) == qk_max
+
+
+def test_granularity_group_maps(orc):
+    """NEXT#4: per-block / per-token group maps partition the tokens as their definitions say."""
+    assert orc.ngroups(0) == (32, 8) and orc.ngroups(1) == (1, 2) and orc.ngroups(2) == (128, 128)
+    assert {orc.group_q_g(t, 1) for t in range(128)} == {0}
+    assert [orc.group_k_g(t, 1) for t in (0, 63, 64, 127, 128)] == [0, 0, 1, 1, 2]
+    assert [orc.group_q_g(t, 2) for t in range(128)] == list(range(128))
+    assert all(orc.group_q_g(t, 0) == orc.group_q(t) for t in range(128))
+    assert all(orc.group_k_g(t, 0) == orc.group_k(t) for t in range(256))
+
+
+def test_per_token_codes_reach_qmax_on_every_row(orc):
+    """With per-token groups every non-zero row has a code of magnitude qmax (its own absmax maps
+    to +-7), unlike per-block groups where only the block's extreme reaches it."""
+    g = np.random.default_rng(5)
+    Qb = (g.standard_normal((128, 64)) * np.exp(g.normal(0, 1, (128, 1)))).astype(np.float16)
+    tok = orc.q_block(Qb, OracleConfig(qk_gran=2))
+    blk = orc.q_block(Qb, OracleConfig(qk_gran=1))
+    assert np.all(np.abs(tok["qhat"]).max(axis=1) == 7)
+    assert len(blk["dq"]) == 1 and np.sum(np.abs(blk["qhat"]).max(axis=1) == 7) < 128
