@@ -71,6 +71,10 @@ extern "C" {
 #define SAGE2_F_SMOOTH_V 32768 /* optional smooth V (NEXT#2): V' = V - V_m before the     */
                                /* per-channel FP8 quantization, O + V_m in the epilogue; pass to    */
                                /* BOTH sage2_prepare and sage2_attention (default kernels only).    */
+#define SAGE2_F_GRAN_BLOCK 262144 /* NEXT#4 ablation: per-block Q/K quantization groups (Q: 128-token */
+                                  /* block, K: 64-token blocks) instead of per-thread  */
+#define SAGE2_F_GRAN_TOKEN 524288 /* NEXT#4 ablation: per-token Q/K quantization groups.  Both flags:  */
+                                  /* d = 128 (v8) only; pass to sage2_prepare AND sage2_attention.    */
 #define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
@@ -115,8 +119,8 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
 /* Workspace layout: writes SAGE2_WS_NREGIONS byte offsets into offsets[] (regions in order:
  * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), vsum(int64 [B*H_kv*d], smooth V),
  * kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]), vmean(f32 [B*H_kv*d], smooth V V_m),
- * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][N_pad/4]), qbar(f32 [B*H_q][nT][d]),
- * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][N_pad/16]),
+ * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][nT][groups]: 32 per-thread groups per block by default; region sized for one per token), qbar(f32 [B*H_q][nT][d]),
+ * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][nT][groups]: 8 per 128 keys by default; sized for one per token),
  * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), qbt(q_bar tf32 big/small split images
  * [B*H_q][ceil(nT/256)][d/32][2][256*128 B], input of the tensor-core Delta S GEMM), ds(f32, scaled
  * by log2(e)/sqrt(d): [B*H_q][nT][N_pad] for non-causal calls; causal calls (SAGE2_F_CAUSAL given to

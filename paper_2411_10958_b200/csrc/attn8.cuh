@@ -30,6 +30,7 @@
 
 #include "attn.cuh"
 #include "attn2.cuh"
+#include "prep.cuh"
 #include "ptx.cuh"
 
 namespace sage2 {
@@ -51,7 +52,9 @@ struct Attn8Smem {
     static constexpr uint32_t ALLOC = BYTES + 1024;
 };
 
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false>
+// GRAN: Q/K quantization granularity of the NEXT#4 ablation (0 per-thread = SageAttn2, 1 per-block,
+// 2 per-token; prep.cuh gran_nq / gran_nk give the stored scales per 128 tokens).
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
 __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     using L = Attn8Smem<D>;
     constexpr int DH = D / 2;                      // output channels per half
@@ -127,10 +130,11 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 if (j >= kStages2) mbar_wait(bar_kv_empty(s), ((j / kStages2) - 1) & 1);
                 const uint32_t sa = stage_addr(s);
                 const bool d0 = j < nkv0, d1 = j < nkv1;
-                mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 32 + 512 * (d0 + d1));
+                constexpr int NGK = gran_nk(GRAN);
+                mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 4 * NGK + 512 * (d0 + d1));
                 bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
                 bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
-                bulk_g2s(sa + L::ST_DK, p.dk + (size_t)bhk * nT * 8 + (size_t)j * 8, 32, bar_kv_full(s));
+                bulk_g2s(sa + L::ST_DK, p.dk + ((size_t)bhk * nT + j) * NGK, 4 * NGK, bar_kv_full(s));
                 if (d0)
                     bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
                 if (d1)
@@ -193,7 +197,8 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             const uint32_t tR = tmem + 128 * k + lane_off + DH * h;      // this half's R channels
             const uint32_t tO = tmem + 256 + D * k + lane_off + DH * h;  // this half's O channels
             const int grow = my_it * 128 + row;
-            const float dqr = p.dq[((size_t)bhq * nT + my_it) * 32 + 8 * (row / 32) + (row % 8)] * p.qk_scale_log2;
+            const float dqr = p.dq[((size_t)bhq * nT + my_it) * gran_nq(GRAN) +
+                                   (GRAN == 2 ? row : GRAN == 1 ? 0 : 8 * (row / 32) + (row % 8))] * p.qk_scale_log2;
             uint8_t* sP = sgen + (k ? L::P1 : L::P0);
             float* xm = reinterpret_cast<float*>(sgen + L::XM) + k * 512;    // [buf][half][128]
             float m = -INFINITY, l = 0.0f;
@@ -207,13 +212,16 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 tc_fence_after();
                 tss(j, 1);
                 const uint32_t dss = stage_addr(s) + (k ? L::ST_DS1 : L::ST_DS0) + 256 * h;
-                const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK) + 4 * h;
+                const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK) +
+                                   (GRAN == 1 ? h : 4 * h);
+                const uint32_t dkv = stage_addr(s) + L::ST_DK + 256 * h;   // per-token delta_K of this half
                 float2 sc2[4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    const float v = dqr * dks[g];
+                    const float v = dqr * dks[GRAN == 1 ? 0 : g];
                     sc2[g] = make_float2(v, v);
                 }
+                const float2 dq2 = make_float2(dqr, dqr);
                 float sv[64];
                 {
                     uint32_t r0[32], r1[32];
@@ -236,10 +244,16 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                         const uint32_t* rr = c < 32 ? r0 : r1;
                         const float4 d4 = lds128(dss + 4 * c);
                         const int g = (c % 8) / 2;
+                        float2 sa2 = sc2[g], sb2 = sc2[g + 1];
+                        if (GRAN == 2) {                     // one delta_K per key column
+                            const float4 k4 = lds128(dkv + 4 * c);
+                            sa2 = fmul2(make_float2(k4.x, k4.y), dq2);
+                            sb2 = fmul2(make_float2(k4.z, k4.w), dq2);
+                        }
                         const float2 a = ffma2(make_float2(s_as_float(rr[c % 32]), s_as_float(rr[c % 32 + 1])),
-                                               sc2[g], make_float2(d4.x, d4.y));
+                                               sa2, make_float2(d4.x, d4.y));
                         const float2 bq = ffma2(make_float2(s_as_float(rr[c % 32 + 2]), s_as_float(rr[c % 32 + 3])),
-                                                sc2[g + 1], make_float2(d4.z, d4.w));
+                                                sb2, make_float2(d4.z, d4.w));
                         sv[c] = a.x;
                         sv[c + 1] = a.y;
                         sv[c + 2] = bq.x;

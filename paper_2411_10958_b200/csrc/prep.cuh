@@ -22,6 +22,14 @@ namespace sage2 {
 
 constexpr int kTile = 128;  // b_q = b_kv = 128 tokens
 
+// Quantization granularity of Q and K (NEXT#4 ablation, oracle qk_gran): 0 per-thread (P:223,
+// SageAttn2), 1 per-block (Q: the 128-token block, K: 64-token blocks), 2 per-token.
+// Groups per 128 tokens (stored layout): Q 32 / 1 / 128, K 8 / 4 (2 used, padded for 16-byte bulk
+// copies) / 128.
+__host__ __device__ constexpr int gran_nq(int gran) { return gran == 1 ? 1 : gran == 2 ? 128 : 32; }
+__host__ __device__ constexpr int gran_nk(int gran) { return gran == 1 ? 4 : gran == 2 ? 128 : 8; }
+
+
 // FP16 bits -> exact integer value * 2^24 (every finite fp16 is a multiple of 2^-24).
 __device__ __forceinline__ long long fp16_fixed24(uint16_t h) {
     int e = (h >> 10) & 31, m = h & 1023;
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(256) k_v_absmax_smooth(const __half* __restric
 //                    in padded shared memory and read back column-wise (thread = channel pair)
 //   dk             : 8 groups per tile (g_K = 4*(t/64) + (t%8)/2)
 // ---------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int GRAN = 0>
 __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ K, const __half* __restrict__ V,
                                                      int N, int qk_max, int e4m3_codes,
                                                      const unsigned long long* __restrict__ ksum,
@@ -291,7 +299,6 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     const int lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     __shared__ float kbar[D], dvs[D];
-    __shared__ float gpart[8][4];
     __shared__ __align__(16) __half vt[kTile * VS];
     const size_t base = (size_t)bh * N * D;
     uint4 kraw[NP];
@@ -316,18 +323,18 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
         }
     }
     __syncthreads();
-    // K' = K - k_bar (O-2), kept in registers; row-pair absmax over the 2*TPR lanes of two rows,
-    // then per group g_K = 4*(r/64) + (r%8)/2 over this leader's passes of the group: leader L =
-    // rofs/2 owns rows 2L, 2L+1 of every pass, group (p*RPP/64, L%4); the RPP/8 leaders of a group
-    // write disjoint slots of gpart (no atomics)
+    // K' = K - k_bar (O-2), kept in registers; absmax per key row -> rowmax, then the group
+    // absmax of the granularity (per-thread group g = rows 64(g/4) + 8k + 2(g%4) + {0, 1},
+    // "K[8k+2i] together with K[8k+2i+1]")
+    __shared__ float rowmax[128];
+    __shared__ float gdelta[128];
     float kx[NP][8];
     float kb[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) kb[i] = kbar[cg * 8 + i];
-    float gm[2] = {0.f, 0.f};
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const int t = tile * kTile + p * RPP + rofs;
+        const int r = p * RPP + rofs, t = tile * kTile + r;
         const __half2* kh2 = reinterpret_cast<const __half2*>(&kraw[p]);
         float m = 0.f;
 #pragma unroll
@@ -338,14 +345,26 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
             m = fmax3(m, fabsf(kx[p][2 * i]), fabsf(kx[p][2 * i + 1]));
         }
 #pragma unroll
-        for (int x = 1; x < 2 * TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
-        gm[(p * RPP) / 64] = fmaxf(gm[(p * RPP) / 64], m);
+        for (int x = 1; x < TPR; x <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, x));
+        if (cg == 0) rowmax[r] = m;
     }
-    constexpr int NSLOT = RPP / 8;
-    const int L = rofs / 2;
-    if (lane % (2 * TPR) == 0) {
-        gpart[L % 4][L / 4] = gm[0];
-        gpart[4 + L % 4][L / 4] = gm[1];
+    __syncthreads();
+    constexpr int NGK = gran_nk(GRAN);
+    if (threadIdx.x < NGK) {
+        const int g = threadIdx.x;
+        float amax = 0.f;
+        if (GRAN == 2) {
+            amax = rowmax[g];
+        } else if (GRAN == 1) {
+            if (g < 2)
+                for (int r = 64 * g; r < 64 * g + 64; ++r) amax = fmaxf(amax, rowmax[r]);
+        } else {
+            const int r0 = 64 * (g / 4) + 2 * (g % 4);
+            for (int k = 0; k < 8; ++k) amax = fmax3(amax, rowmax[r0 + 8 * k], rowmax[r0 + 8 * k + 1]);
+        }
+        const float delta = __fdiv_rn(amax, (float)qk_max);
+        gdelta[g] = delta;
+        dk[((size_t)bh * nT + tile) * NGK + g] = delta;
     }
     __syncthreads();
     // K codes (O-3) straight to the swizzled K^ tile image
@@ -353,20 +372,10 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const int g = 4 * (r / 64) + (r % 8) / 2;
-        float amax = gpart[g][0];
-#pragma unroll
-        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[g][k]);
-        const float delta = __fdiv_rn(amax, (float)qk_max);
+        const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 ? r / 64 : 4 * (r / 64) + (r % 8) / 2];
         int code[8];
         quant_codes8(kx[p], delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
-    }
-    if (threadIdx.x < 8) {
-        float amax = gpart[threadIdx.x][0];
-#pragma unroll
-        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[threadIdx.x][k]);
-        dk[(size_t)bh * (nT * 8) + tile * 8 + threadIdx.x] = __fdiv_rn(amax, (float)qk_max);
     }
     // V codes (O-4): thread = channel pair (c, c+1) x TOK consecutive tokens -> V^T rows c, c+1
     constexpr int NPAIR = D / 2, TOK = kTile / (256 / NPAIR);
@@ -410,24 +419,21 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 //  * exact means in fp64: 128 fp16 values are multiples of 2^-24 below 2^23 in magnitude, so every
 //    partial sum fits 47 bits and the fp64 sum is exact in any order -- bit-identical to the int64
 //    fixed-point sum of reading C-1 (and 8x fewer instructions than the fixed-point conversion);
-//  * the group absmax without atomics: a thread's rows of one group are combined in registers, the
-//    (2 or 4) contributing threads of a group write disjoint slots of gpart;
+//  * the group absmax without atomics: per-row maxima in shared memory, one thread per group;
 //  * gamma(Q) is computed once and kept in registers for the quantizer.
 // ---------------------------------------------------------------------------------------------
 
-template <int D>
+template <int D, int GRAN = 0>
 __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
                                                     float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // d=128: 16 / 16 / 8; d=64: 8 / 32 / 4
-    constexpr int NSLOT = RPP / 8;                                   // contributors per group (2 / 4)
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     const int n = min(kTile, N - tile * kTile);          // present tokens (C-18)
     __shared__ double part[8][D];
     __shared__ float qbar[D];
-    __shared__ float gpart[32][4];
     const size_t base = (size_t)bh * N * D;
     uint4 raw[NP];
 #pragma unroll
@@ -472,13 +478,15 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
         *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qb, big);
     }
     __syncthreads();
-    // gamma(Q) (O-5) kept in registers; absmax per row (over the TPR lanes of the row), then per
-    // group over this thread's rows of the group (rows p with equal p / (NP/4))
+    // gamma(Q) (O-5) kept in registers; absmax per row (over the TPR lanes of the row) -> rowmax,
+    // then the group absmax of the granularity from rowmax (per-thread group g = rows
+    // 32(g/8) + g%8 + 8k, k < 4, "tokens i, 8+i, 16+i, 24+i")
+    __shared__ float rowmax[128];
+    __shared__ float gdelta[128];
     float x[NP][8];
     float qv[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) qv[i] = qbar[cg * 8 + i];
-    float gm[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
@@ -493,32 +501,35 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
         }
 #pragma unroll
         for (int o = 1; o < TPR; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        gm[p / (NP / 4)] = fmaxf(gm[p / (NP / 4)], m);
+        if (cg == 0) rowmax[r] = m;
     }
-    // group of (p, rofs): 8 * (r / 32) + r % 8 with r / 32 = p / (NP / 4), r % 8 = rofs % 8
-    if (cg == 0) {
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) gpart[8 * c4 + rofs % 8][rofs / 8] = gm[c4];
+    __syncthreads();
+    constexpr int NGQ = gran_nq(GRAN);
+    if (threadIdx.x < NGQ) {
+        const int g = threadIdx.x;
+        float amax;
+        if (GRAN == 2) {
+            amax = rowmax[g];
+        } else if (GRAN == 1) {
+            amax = 0.f;
+            for (int r = 0; r < 128; ++r) amax = fmaxf(amax, rowmax[r]);
+        } else {
+            const int r0 = 32 * (g / 8) + g % 8;
+            amax = fmaxf(fmaxf(rowmax[r0], rowmax[r0 + 8]), fmaxf(rowmax[r0 + 16], rowmax[r0 + 24]));
+        }
+        const float delta = __fdiv_rn(amax, (float)qk_max);   // O-6
+        gdelta[g] = delta;
+        dq[((size_t)bh * nT + tile) * NGQ + g] = delta;
     }
     __syncthreads();
     int8_t* img = qhat + ((size_t)bh * nT + tile) * (size_t)kTile * D;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const int g = 8 * (r / 32) + (r % 8);
-        float amax = gpart[g][0];
-#pragma unroll
-        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[g][k]);
-        const float delta = __fdiv_rn(amax, (float)qk_max);   // O-6
+        const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 ? 0 : 8 * (r / 32) + (r % 8)];
         int code[8];
         quant_codes8(x[p], delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
-    }
-    if (threadIdx.x < 32) {
-        float amax = gpart[threadIdx.x][0];
-#pragma unroll
-        for (int k = 1; k < NSLOT; ++k) amax = fmaxf(amax, gpart[threadIdx.x][k]);
-        dq[((size_t)bh * nT + tile) * 32 + threadIdx.x] = __fdiv_rn(amax, (float)qk_max);
     }
 }
 

@@ -73,10 +73,10 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
         BHk * d * 4,          // dv
         BHk * d * 4,          // vmean (smooth V)
         BHq * Np * d,         // qhat
-        BHq * (Np / 4) * 4,   // dq
+        BHq * Np * 4,         // dq (up to one scale per token: per-token granularity)
         BHq * nT * d * 4,     // qbar
         BHk * Np * d,         // khat
-        BHk * (Np / 16) * 4,  // dk
+        BHk * Np * 4,         // dk (up to one scale per token)
         BHk * Np * d,         // vhat
         BHq * ((nT + 255) / 256) * (size_t)(d / 32) * 65536,   // qbt (q_bar tf32 split images)
         // ds last (its size is the only one that depends on causal): full [nT][N_pad] rows, or the
@@ -101,6 +101,10 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 bool flags_ok(int flags) {
     const int kernels = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
                         SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING;
+    // granularity ablation (NEXT#4): v8 only (no carrier, no kernel selector), not both flags
+    const int granf = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
+    if ((flags & granf) == granf) return false;
+    if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | kernels | SAGE2_F_KERNEL_V6))) return false;
     // smooth V: the epilogue "+ V_m" exists in the default kernels (v6, v8) only
     if ((flags & SAGE2_F_SMOOTH_V) && (flags & (kernels & ~SAGE2_F_DEBUG_TIMING))) return false;
     return !((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | kernels)));
@@ -128,13 +132,17 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     } else {
         k_kv_stats<D, false><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
     }
-    k_kv_quant<D><<<dim3(nT, BHk), 256, 0, st>>>(
+    const int gran = (flags & SAGE2_F_GRAN_TOKEN) ? 2 : (flags & SAGE2_F_GRAN_BLOCK) ? 1 : 0;
+    auto kvq = gran == 2 ? k_kv_quant<D, 2> : gran == 1 ? k_kv_quant<D, 1> : k_kv_quant<D, 0>;
+    auto qq = gran == 2 ? k_q_quant<D, 2> : gran == 1 ? k_q_quant<D, 1> : k_q_quant<D, 0>;
+    kvq<<<dim3(nT, BHk), 256, 0, st>>>(
         k, v, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
         reinterpret_cast<float*>(ws + L.off[R_DK]), ws + L.off[R_VHAT], reinterpret_cast<float*>(ws + L.off[R_KBAR]),
         reinterpret_cast<float*>(ws + L.off[R_DV]), smv ? vmean : nullptr);
-    k_q_quant<D><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, smooth_q, reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
-                                                reinterpret_cast<float*>(ws + L.off[R_DQ]),
-                                                reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
+    qq<<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, smooth_q,
+                                      reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
+                                      reinterpret_cast<float*>(ws + L.off[R_DQ]),
+                                      reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     if (flags & SAGE2_F_DS_SIMT) {
         k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
@@ -224,18 +232,18 @@ int launch_attn6_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false>
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
 int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn8Smem<D>;
     constexpr uint32_t smem = L::ALLOC;
     static bool configured = false;
     if (!configured) {
-        if (cudaFuncSetAttribute(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
             return cuda_rc();
         configured = true;
     }
-    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
+    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
     return cuda_rc();
 }
 
@@ -312,6 +320,14 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     if ((flags & SAGE2_F_KERNEL_V8) || (d == 128 && !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1)))) {
         // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
         const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;
+        if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
+            if (d != 128 || s_dump) return SAGE2_EINVAL;
+            if (flags & SAGE2_F_GRAN_TOKEN)
+                return causal ? launch_attn8_t<128, true, false, false, false, 2>(p, B, st)
+                              : launch_attn8_t<128, false, false, false, false, 2>(p, B, st);
+            return causal ? launch_attn8_t<128, true, false, false, false, 1>(p, B, st)
+                          : launch_attn8_t<128, false, false, false, false, 1>(p, B, st);
+        }
         if (flags & SAGE2_F_DEBUG_TIMING) {
             if (d == 64) return launch_attn8_t<64, false, false, false, true>(p, B, st);
             return launch_attn8_t<128, false, false, false, true>(p, B, st);

@@ -87,11 +87,12 @@ def _check_inputs(q, k, v):
 
 F_QK_E4M3 = 2048    # include/sage2.h SAGE2_F_QK_E4M3 (E4M3-carrier QK^T variant)
 F_SMOOTH_V = 32768  # include/sage2.h SAGE2_F_SMOOTH_V (optional smooth V)
+F_GRAN = {"thread": 0, "block": 262144, "token": 524288}   # SAGE2_F_GRAN_* (NEXT#4 ablation)
 
 
-def flags(causal=False, int8=False, qk_e4m3=False, smooth_v=False):
+def flags(causal=False, int8=False, qk_e4m3=False, smooth_v=False, gran="thread"):
     return ((F_CAUSAL if causal else 0) | (F_INT8 if int8 else 0) | (F_QK_E4M3 if qk_e4m3 else 0) |
-            (F_SMOOTH_V if smooth_v else 0))
+            (F_SMOOTH_V if smooth_v else 0) | F_GRAN[gran])
 
 
 def workspace_bytes(B, Hq, Hkv, N, d, causal=False):
@@ -110,22 +111,24 @@ def alloc_workspace(B, Hq, Hkv, N, d, device="cuda", causal=False):
     return torch.empty(workspace_bytes(B, Hq, Hkv, N, d, causal), dtype=torch.uint8, device=device)
 
 
-def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=False, smooth_v=False):
+def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=False, smooth_v=False,
+         gran="thread"):
     """SageAttn2 forward: q [B,Hq,N,d], k/v [B,Hkv,N,d] fp16 CUDA -> out [B,Hq,N,d] fp16.
     qk_e4m3=True runs QK^T through the E4M3 carrier (kind::f8f6f4) instead of kind::i8;
-    smooth_v=True subtracts V's column mean before the FP8 quantization and adds it back."""
+    smooth_v=True subtracts V's column mean before the FP8 quantization and adds it back (P:304-306);
+    gran="block"/"token" selects the granularity-ablation quantization groups (d = 128 only)."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     if out is None:
         out = torch.empty_like(q)
-    if workspace is None and not int8 and not qk_e4m3 and not smooth_v:
+    if workspace is None and not int8 and not qk_e4m3 and not smooth_v and gran == "thread":
         _check(lib().sage2_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
                                 int(causal), _stream()))
         return out
     if workspace is None:
         workspace = alloc_workspace(B, Hq, Hkv, N, d, q.device)
     _check(lib().sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
-                               flags(causal, int8, qk_e4m3, smooth_v), workspace.data_ptr(), workspace.numel(),
+                               flags(causal, int8, qk_e4m3, smooth_v, gran), workspace.data_ptr(), workspace.numel(),
                                _stream()))
     return out
 
@@ -133,14 +136,15 @@ def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=Fa
 DS_SIMT = 1024      # include/sage2.h SAGE2_F_DS_SIMT
 
 
-def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3=False, smooth_v=False):
+def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3=False, smooth_v=False,
+            gran="thread"):
     """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`.
 
     ds_simt=True computes Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM
     (A/B checks)."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
-    fl = flags(causal, int8, qk_e4m3, smooth_v) | (DS_SIMT if ds_simt else 0)
+    fl = flags(causal, int8, qk_e4m3, smooth_v, gran) | (DS_SIMT if ds_simt else 0)
     _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
@@ -149,12 +153,12 @@ KERNEL_FLAGS = {"default": 0, "v6": 8192, "v8": 4096, "v1": 128, "v5": 512, "v4"
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
-              smooth_v=False):
+              smooth_v=False, gran="thread"):
     """The tcgen05 attention kernel only, on a prepared workspace (kernel: default = v8 for d=128 and
     v6 for d=64, or an A/B variant;
     qk_e4m3 must match the prepare() call)."""
     _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
-                                 flags(causal, int8, qk_e4m3, smooth_v) | KERNEL_FLAGS[kernel],
+                                 flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
     return out
 

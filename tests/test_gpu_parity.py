@@ -21,7 +21,7 @@ import torch
 import oracle as orc
 from oracle import OracleConfig
 from paper_2411_10958_b200 import sage2, synth
-from tests._gpu_helpers import fp16_ulp, read_prepared, to_np16
+from tests._gpu_helpers import fp16_ulp, read_prepared, region, to_np16
 
 pytestmark = pytest.mark.gpu
 
@@ -359,3 +359,39 @@ def test_causal_compact_delta_s(N, d):
             assert np.array_equal(got.view(np.uint32), full[bh, i, :128 * (i + 1)].view(np.uint32))
     # config C4 (Llama-3.1-8B-like, N = 100000 causal): 10.7 GB -> 5.7 GB of workspace
     assert sage2.workspace_bytes(1, 32, 8, 100000, 128, causal=True) < 0.55 * sage2.workspace_bytes(1, 32, 8, 100000, 128)
+
+
+@pytest.mark.parametrize("gran", ["block", "token"])
+@pytest.mark.parametrize("B,Hq,Hkv,N,causal", [(1, 2, 1, 300, False), (2, 4, 2, 384, True)])
+def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
+    """NEXT#4: per-block / per-token Q/K groups.  Codes and scales bit-exact against the oracle's
+    qk_gran, outputs within the same bar as the default (d = 128, kernel v8)."""
+    d = 128
+    gi = {"block": 1, "token": 2}[gran]
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=21)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws, causal=causal, gran=gran)
+    out = torch.empty_like(qg)
+    sage2.attention(out, ws, B, Hq, Hkv, N, d, causal=causal, gran=gran)
+    torch.cuda.synchronize()
+    lay = sage2.layout(B, Hq, Hkv, N, d)
+    g = read_prepared(ws, lay, B, Hq, Hkv, N, d)
+    nT = (N + 127) // 128
+    nq, nk = orc.ngroups(gi)
+    nk_store = 4 if gi == 1 else nk
+    dq = region(ws, lay, "dq", np.float32, B * Hq * nT * nq).reshape(B * Hq, nT, nq)
+    dk = region(ws, lay, "dk", np.float32, B * Hkv * nT * nk_store).reshape(B * Hkv, nT, nk_store)
+    cfg = OracleConfig(causal=causal, qk_gran=gi)
+    for b in range(B):
+        for hk in range(Hkv):
+            kv = orc.kv_head(k.numpy()[b, hk], v.numpy()[b, hk], cfg)
+            assert np.array_equal(g["khat"][b * Hkv + hk], kv["khat"])
+            assert np.array_equal(dk[b * Hkv + hk, :, :nk].reshape(-1).view(np.uint32), kv["dk"].view(np.uint32))
+        for hq in range(Hq):
+            for i in range(nT):
+                qb = orc.q_block(q.numpy()[b, hq, 128 * i:min(N, 128 * i + 128)], cfg)
+                assert np.array_equal(g["qhat"][b * Hq + hq, 128 * i:128 * i + 128], qb["qhat"])
+                assert np.array_equal(dq[b * Hq + hq, i].view(np.uint32), qb["dq"].view(np.uint32))
+    units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+    _compare_out(to_np16(out).astype(np.float64), res, units, N)
