@@ -106,7 +106,7 @@ int sage2_attn_ex(const void* q, const void* k, const void* v, void* out, int B,
                   int d, int flags, void* workspace, size_t ws_bytes, void* stream);
 
 /* End-to-end call on HOST buffers (page-locked memory required for copy/compute overlap; same
- * layouts as above).  Pipelined over up to 8 chunks of (b, h_kv) units on two internal streams:
+ * layouts as above).  Pipelined over up to 16 chunks of (b, h_kv) units on two internal streams:
  * each chunk's H2D copy, preprocessing, attention and D2H copy are stream-ordered, so one chunk's
  * copies overlap the other's kernels.  Device buffers (two chunk sets) are allocated and freed
  * stream-ordered on `stream`.  Asynchronous like every other entry point: the caller synchronizes

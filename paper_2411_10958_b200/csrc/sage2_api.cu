@@ -97,6 +97,38 @@ enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KH
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Library-owned stream-ordered memory pool of the current device for the internal allocations of
+// sage2_attn / sage2_attn_host (workspace, host-path device buffers).  Its release threshold is
+// unlimited, so freed blocks stay mapped for the next call instead of being unmapped and re-mapped
+// (gigabytes per call).  The process's default pool and torch's allocator are not touched.
+cudaMemPool_t lib_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!pools[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = pool;
+    }
+    return pools[dev];
+}
+
+cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool = lib_pool();
+    return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
+}
+
 // The E4M3 carrier only holds the INT4 codes (|c| <= 7) and exists only in the default kernel.
 bool flags_ok(int flags) {
     const int kernels = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
@@ -501,7 +533,7 @@ int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, in
     const size_t bytes = sage2_workspace_bytes(B, H_q, H_kv, N, d, causal);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     void* ws = nullptr;
-    if (cudaMallocAsync(&ws, bytes, st) != cudaSuccess) {
+    if (lib_malloc_async(&ws, bytes, st) != cudaSuccess) {
         cudaGetLastError();
         return SAGE2_ENOMEM;
     }
@@ -521,7 +553,7 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q_host || !k_host || !v_host || !out_host) return SAGE2_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int grp = H_q / H_kv, units = B * H_kv;
-    int nch = units < 8 ? units : 8;
+    int nch = units < 16 ? units : 16;
     const int U = (units + nch - 1) / nch;                 // units per chunk
     nch = (units + U - 1) / U;
     const size_t qu = (size_t)grp * N * d * 2, ku = (size_t)N * d * 2;   // bytes per unit
@@ -537,7 +569,7 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
             bad();
         const size_t sz[5] = {U * qu, U * ku, U * ku, U * qu, wsb};
         for (int r = 0; r < 5 && rc == SAGE2_OK; ++r)
-            if (cudaMallocAsync(&buf[i][r], sz[r], st) != cudaSuccess) {
+            if (lib_malloc_async(&buf[i][r], sz[r], st) != cudaSuccess) {
                 cudaGetLastError();
                 rc = SAGE2_ENOMEM;
             }
