@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
 
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // warp index through a shuffle: provably warp-uniform, so everything derived from it (role,
+    // tile, half, TMEM / shared addresses) can live in uniform registers instead of being
+    // rematerialised from threadIdx every iteration under the softmax warps' register pressure
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
     const int wg = warp / 4;
     const int nT = p.nT, Np = nT * 128;
     const int npairs = (nT + 1) / 2;
