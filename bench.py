@@ -315,8 +315,7 @@ def run_ours(args, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
         "data": "synthetic", "config": workload_config(name),
         "gpu_launches": 5 * args.steps,
-        "roofline": {"bound": "tensor", "kernel": ("k_attn8 (tcgen05 attention, v8)" if d == 128 else
-                                                          "k_attn6 (tcgen05 attention, v6)"), "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": "k_attn8 (tcgen05 attention, v8)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms_max,
                      "kernel_share_of_step": kms_max / ms_max},

@@ -53,8 +53,7 @@ extern "C" {
 #define SAGE2_F_INT8 2     /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing,  */
                            /* P:70, P:476 (Table 3)                                    */
 #define SAGE2_F_KERNEL_V0 4 /* use the simple one-Q-tile-per-CTA attention kernel (A/B checks)  */
-/* Kernel variants (A/B timing and parity).  Default: v8 (csrc/attn8.cuh) for d = 128, v6         */
-/* (csrc/attn6.cuh) for d = 64; both b_kv = 128.                                                  */
+/* Kernel variants (A/B timing and parity).  Default: v8 (csrc/attn8.cuh), b_kv = 128.            */
 #define SAGE2_F_KERNEL_V4 8 /* use the experimental v4 kernel (one Q tile / CTA, column-split     */
                             /* softmax warpgroups, triple-buffered S/R in TMEM)                    */
 #define SAGE2_F_DEBUG_NULLSM 16 /* v4 timing experiment: skip softmax work (output is NOT attention)*/
@@ -65,7 +64,7 @@ extern "C" {
 #define SAGE2_F_QK_E4M3 2048 /* E4M3-carrier QK^T: INT4 codes stored as E4M3 bytes, S on kind::f8f6f4 */
                              /* (fp32 accumulator, same integer S); pass to BOTH sage2_prepare and  */
                              /* sage2_attention.  Invalid with SAGE2_F_INT8 or a KERNEL flag.       */
-#define SAGE2_F_KERNEL_V6 8192 /* force the v6 kernel for d = 128 (A/B)                             */
+#define SAGE2_F_KERNEL_V6 8192 /* use the v6 kernel (one softmax warpgroup per Q tile; A/B)           */
 #define SAGE2_F_KERNEL_V8 4096 /* use the v8 kernel (v6 with each Q tile's softmax split over two   */
                                /* warpgroups by key columns: 4 softmax warps per SM sub-partition) */
 #define SAGE2_F_SMOOTH_V 32768 /* optional smooth V (NEXT#2): V' = V - V_m before the     */

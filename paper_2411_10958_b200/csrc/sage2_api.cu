@@ -347,9 +347,8 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
         return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
     }
-    // default for d = 128: v8 (measured 1119 vs 1059 TOPS non-causal, 1101 vs 1023 causal at C2-32K);
-    // d = 64 keeps v6 (640 vs 601): its tiles are too small to pay for the max exchange.
-    if ((flags & SAGE2_F_KERNEL_V8) || (d == 128 && !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1)))) {
+    // default: v8 (C2-32K: d=128 1212 vs 1059 TOPS for v6, causal 1190 vs 1023; d=64 658 vs 644)
+    if ((flags & SAGE2_F_KERNEL_V8) || !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1))) {
         // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
         const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;
         if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
@@ -388,7 +387,8 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
                       : launch_attn6_t<128, false, false, false, true>(p, B, st);
     }
     if (!(flags & SAGE2_F_KERNEL_V1)) {
-        // v6 (default for d = 64) -- b_kv = 128, two Q tiles, promotion in the softmax warps, MUFU ping-pong
+        // v6 (SAGE2_F_KERNEL_V6, and the E4M3-carrier path) -- b_kv = 128, two Q tiles, one softmax
+        // warpgroup per tile, promotion in the softmax warps, MUFU ping-pong
         if (flags & SAGE2_F_DEBUG_TIMING) {
             if (d == 64) return launch_attn6_t<64, false, false, true>(p, B, st);
             return launch_attn6_t<128, false, false, true>(p, B, st);
