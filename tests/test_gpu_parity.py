@@ -395,3 +395,28 @@ def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
+
+
+def test_random_shapes_fuzz():
+    """Randomised shapes and flags (seeded): B, H_q/H_kv (GQA), ragged N (1..700), d, causal,
+    input kind, smooth V and the INT8 variant -- every case held to the oracle bar."""
+    rng = np.random.default_rng(2024)
+    for case in range(12):
+        d = int(rng.choice([64, 128]))
+        Hkv = int(rng.integers(1, 3))
+        Hq = Hkv * int(rng.choice([1, 2, 4]))
+        B = int(rng.integers(1, 3))
+        N = int(rng.integers(1, 701))
+        causal = bool(rng.integers(0, 2))
+        kind = str(rng.choice(["iid", "structured"]))
+        smooth_v = bool(rng.integers(0, 2))
+        int8 = (not smooth_v) and bool(rng.integers(0, 4) == 0)
+        q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=100 + case)
+        out = sage2.attn(qg, kg, vg, causal=causal, int8=int8, smooth_v=smooth_v)
+        torch.cuda.synchronize()
+        units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
+        cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8)
+        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+        err, cos, flipped = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+        print(f"case {case}: B={B} Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} sv={smooth_v} "
+              f"int8={int8}: max|err|={err:.2e} cos={cos:.7f}")
