@@ -19,7 +19,11 @@
  * quantizer fixed points and endpoints, the paper's group examples, exact mode vs
  * an independent dense numpy softmax-attention, smoothing invariance, two-level ==
  * single-level in fp64, single tile == dense per-tile formula, brute force on tiny
- * inputs by a second naive Python implementation, and the lossless special case.
+ * inputs by a second naive Python implementation (per-thread, per-block and per-token groups), the
+ * lossless special case, smooth V (constant V is reproduced exactly), and the paper's
+ * directions (smoothing and granularity accuracy orderings, two-level under FP22).
+ * Parity unpinned: the paper's accuracy NUMBERS (CosSim / Rel-L1 / RMSE on real CogVideoX tensors,
+ * P:499-547) -- synthetic inputs can only pin their orderings.
  */
 #include <math.h>
 #include <stdint.h>
