@@ -107,3 +107,14 @@ def test_metrics_properties(orc):
     assert orc.cos_sim(o, 3.0 * o) == pytest.approx(1.0, abs=1e-15)
     assert orc.rel_l1(o, 2 * o) == pytest.approx(1.0, abs=1e-15)
     assert orc.rmse(2 * o, 2 * (o + 1)) == pytest.approx(2.0, abs=1e-12)
+
+
+def test_accuracy_metric_definitions(orc):
+    """P:895 metrics on hand-computable vectors: CosSim of parallel / orthogonal vectors, Rel-L1 =
+    sum|O - O'| / sum|O|, RMSE = sqrt(mean (O - O')^2)."""
+    a = np.array([1.0, 2.0, 2.0])
+    assert abs(orc.cos_sim(a, 3 * a) - 1.0) < 1e-15
+    assert abs(orc.cos_sim(np.array([1.0, 0.0]), np.array([0.0, 5.0]))) < 1e-15
+    b = np.array([1.0, 1.0, 4.0])                      # |a - b| = (0, 1, 2)
+    assert abs(orc.rel_l1(a, b) - 3.0 / 5.0) < 1e-15
+    assert abs(orc.rmse(a, b) - np.sqrt(5.0 / 3.0)) < 1e-15
