@@ -105,9 +105,9 @@ int sage2_attn_ex(const void* q, const void* k, const void* v, void* out, int B,
                   int d, int flags, void* workspace, size_t ws_bytes, void* stream);
 
 /* End-to-end call on HOST buffers (page-locked memory required for copy/compute overlap; same
- * layouts as above).  Pipelined over up to 16 chunks of (b, h_kv) units on two internal streams:
+ * layouts as above).  Pipelined over up to 16 chunks of (b, h_kv) units on three internal streams:
  * each chunk's H2D copy, preprocessing, attention and D2H copy are stream-ordered, so one chunk's
- * copies overlap the other's kernels.  Device buffers (two chunk sets) are allocated and freed
+ * copies overlap the others' kernels.  Device buffers (three chunk sets) are allocated and freed
  * stream-ordered on `stream`.  Asynchronous like every other entry point: the caller synchronizes
  * `stream` before reading out.  Errors: SAGE2_EINVAL, SAGE2_ENOMEM, SAGE2_ECUDA. */
 int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, void* out_host, int B, int H_q,
