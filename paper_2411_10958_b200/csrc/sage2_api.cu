@@ -153,7 +153,11 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return cuda_rc();
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
-    const int rows_per_cta = 512;
+    // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
+    // ~4 CTAs per SM (1K tokens: 22 -> ~10 us).  fp64 in-CTA sums stay exact up to 8192 rows.
+    int rows_per_cta = 512;
+    while (rows_per_cta > 64 && (long long)((N + rows_per_cta - 1) / rows_per_cta) * (long long)BHk < 4LL * 148)
+        rows_per_cta /= 2;
     const bool smv = (flags & SAGE2_F_SMOOTH_V) != 0;
     auto* vsum = reinterpret_cast<unsigned long long*>(ws + L.off[R_VSUM]);
     auto* vmean = reinterpret_cast<float*>(ws + L.off[R_VMEAN]);
@@ -176,7 +180,10 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
                                       reinterpret_cast<float*>(ws + L.off[R_DQ]),
                                       reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-    if (flags & SAGE2_F_DS_SIMT) {
+    // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
+    // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
+    // oracle by the same bound.
+    if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
         k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                     reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
                                                     scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
