@@ -420,3 +420,30 @@ def test_random_shapes_fuzz():
         err, cos, flipped = _compare_out(to_np16(out).astype(np.float64), res, units, N)
         print(f"case {case}: B={B} Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} sv={smooth_v} "
               f"int8={int8}: max|err|={err:.2e} cos={cos:.7f}")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_delta_s_tensor_core_path(causal):
+    """Delta S on the persistent tf32 tcgen05 GEMM (used for N > 2048; shorter sequences take the
+    SIMT kernel): sampled rows against the oracle's fp64 sum, same bound as test_preprocess_bit_exact,
+    in the full and the triangular causal layouts."""
+    B, Hq, Hkv, N, d = 1, 2, 1, 4500, 128
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=19)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d, causal=causal)
+    sage2.prepare(qg, kg, vg, ws, causal=causal)
+    torch.cuda.synchronize()
+    lay = sage2.layout(B, Hq, Hkv, N, d)
+    nT = (N + 127) // 128
+    Np = nT * 128
+    n_ds = B * Hq * (64 * nT * (nT + 1) if causal else nT * Np)
+    ds = region(ws, lay, "ds", np.float32, n_ds)
+    kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
+    for h in range(Hq):
+        for i in (0, nT // 2, nT - 1):
+            qb = orc.q_block(q.numpy()[0, h, 128 * i:min(N, 128 * i + 128)])
+            ref = orc.delta_s(qb["qbar"], kv["kprime"])
+            keys = min(N, 128 * (i + 1)) if causal else N
+            off = h * 64 * nT * (nT + 1) + 64 * i * (i + 1) if causal else (h * nT + i) * Np
+            got = ds[off:off + keys].astype(np.float64) / (LOG2E / math.sqrt(d))
+            bound = 2e-6 * (np.abs(kv["kprime"][:keys]).astype(np.float64) @ np.abs(qb["qbar"]).astype(np.float64))
+            assert np.all(np.abs(got - ref[:keys]) <= bound + 1e-6 * np.abs(ref[:keys]) + 1e-30)
