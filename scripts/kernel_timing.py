@@ -18,7 +18,7 @@ buf = torch.zeros(3 * 64 * 16, dtype=torch.int64, device="cuda")
 L = sage2.lib()
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(3):
-    rc = L.sage2_debug_qk_int32(out.data_ptr(), buf.data_ptr(), None, B, H, H, N, d, 64, ws.data_ptr(),
+    rc = L.sage2_debug_qk_int32(out.data_ptr(), buf.data_ptr(), None, B, H, H, N, d, 64 + 8, ws.data_ptr(),
                                 ctypes.c_size_t(ws.numel()), st)
     assert rc == 0, L.sage2_last_cuda_error()
 torch.cuda.synchronize()

@@ -1,5 +1,5 @@
 """Per-phase clock64 stamps of one CTA of the v6 / v8 attention kernel (SAGE2_F_DEBUG_TIMING;
-flags argument 64 = v6, 64 + 4096 = v8).
+flags argument 64 + 8192 = v6 (default), 64 + 4096 = v8; scripts/kernel_timing_v8.py has the v8 layout).
 
 Slots (softmax tile k, lane 0 of its first warp): 0 loop start, 1 S ready, 2 S loaded + dequant,
 3 max done, 4 MUFU turn acquired, 5 P^ written, 6 R ready, 7 R read (S/R freed), 8 promotion done.
@@ -17,7 +17,7 @@ from paper_2411_10958_b200 import sage2, synth  # noqa: E402
 B, H = 1, 4
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-flags = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+flags = int(sys.argv[3]) if len(sys.argv) > 3 else 64 + 8192   # DEBUG_TIMING | KERNEL_V6
 q, k, v = synth.make_qkv(B, H, H, N, d, device="cuda")
 ws = sage2.alloc_workspace(B, H, H, N, d)
 sage2.prepare(q, k, v, ws)
