@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 // ---------------------------------------------------------------------------------------------
 
 template <int D, int GRAN = 0>
-__global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
+__global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
                                                     float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // d=128: 16 / 16 / 8; d=64: 8 / 32 / 4
@@ -478,27 +478,33 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
         *reinterpret_cast<float*>(img + 256 * 128 + off) = __fsub_rn(qb, big);
     }
     __syncthreads();
-    // gamma(Q) (O-5) kept in registers; absmax per row (over the TPR lanes of the row) -> rowmax,
-    // then the group absmax of the granularity from rowmax (per-thread group g = rows
+    // gamma(Q) (O-5), recomputed from the raw fp16 in both passes (cheaper than holding 8 x NP
+    // floats: fewer registers, more CTAs in flight); absmax per row (over the TPR lanes of the row)
+    // -> rowmax, then the group absmax of the granularity from rowmax (per-thread group g = rows
     // 32(g/8) + g%8 + 8k, k < 4, "tokens i, 8+i, 16+i, 24+i")
     __shared__ float rowmax[128];
     __shared__ float gdelta[128];
-    float x[NP][8];
     float qv[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) qv[i] = qbar[cg * 8 + i];
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
+    auto gamma8 = [&](int p, float (&x)[8]) {
         const int r = p * RPP + rofs;
         const __half2* h2 = reinterpret_cast<const __half2*>(&raw[p]);
-        float m = 0.f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float2 f = __half22float2(h2[i]);
-            x[p][2 * i] = (r < n) ? __fsub_rn(f.x, qv[2 * i]) : 0.0f;
-            x[p][2 * i + 1] = (r < n) ? __fsub_rn(f.y, qv[2 * i + 1]) : 0.0f;
-            m = fmax3(m, fabsf(x[p][2 * i]), fabsf(x[p][2 * i + 1]));
+            x[2 * i] = (r < n) ? __fsub_rn(f.x, qv[2 * i]) : 0.0f;
+            x[2 * i + 1] = (r < n) ? __fsub_rn(f.y, qv[2 * i + 1]) : 0.0f;
         }
+    };
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const int r = p * RPP + rofs;
+        float x[8];
+        gamma8(p, x);
+        float m = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) m = fmax3(m, fabsf(x[2 * i]), fabsf(x[2 * i + 1]));
 #pragma unroll
         for (int o = 1; o < TPR; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (cg == 0) rowmax[r] = m;
@@ -527,8 +533,10 @@ __global__ void __launch_bounds__(256, 3) k_q_quant(const __half* __restrict__ Q
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
         const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 ? 0 : 8 * (r / 32) + (r % 8)];
+        float x[8];
+        gamma8(p, x);
         int code[8];
-        quant_codes8(x[p], delta, __frcp_rn(delta), qk_max, code);
+        quant_codes8(x, delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(img + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
     }
 }
