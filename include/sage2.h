@@ -67,6 +67,7 @@ extern "C" {
 #define SAGE2_F_KERNEL_V6 8192 /* use the v6 kernel (one softmax warpgroup per Q tile; A/B)           */
 #define SAGE2_F_KERNEL_V8 4096 /* use the v8 kernel (v6 with each Q tile's softmax split over two   */
                                /* warpgroups by key columns: 4 softmax warps per SM sub-partition) */
+                               /* No kernel flag: v10 for d = 128, non-causal, N <= 8192, else v8.  */
 #define SAGE2_F_SMOOTH_V 32768 /* optional smooth V (NEXT#2): V' = V - V_m before the     */
                                /* per-channel FP8 quantization, O + V_m in the epilogue; pass to    */
                                /* BOTH sage2_prepare and sage2_attention (default kernels only).    */
@@ -75,6 +76,8 @@ extern "C" {
 #define SAGE2_F_GRAN_TOKEN 524288 /* NEXT#4 ablation: per-token Q/K quantization groups.  Both flags:  */
                                   /* d = 128 (v8) only; pass to sage2_prepare AND sage2_attention.    */
 #define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
+#define SAGE2_F_KERNEL_V10 16384 /* use the v10 kernel: v8 made persistent (one CTA per SM looping over */
+                                /* (Q-block pair, h_q, b) items); not with QK_E4M3/GRAN/TIMING: EINVAL */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
 const char* sage2_last_cuda_error(void);
@@ -116,6 +119,7 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
 /* ---- staged entry points (the same kernels, split so each stage can be timed / inspected) ---- */
 
 /* Workspace layout: writes SAGE2_WS_NREGIONS byte offsets into offsets[] (regions in order:
+ * sched(256 B: the v10 kernel's work-item counters, zeroed by sage2_prepare, reset by the kernel),
  * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), vsum(int64 [B*H_kv*d], smooth V),
  * kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]), vmean(f32 [B*H_kv*d], smooth V V_m),
  * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][nT][groups]: 32 per-thread groups per block by default; region sized for one per token), qbar(f32 [B*H_q][nT][d]),
@@ -128,7 +132,7 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
  * the non-causal ones (identical except end).  Tile images are K-major, 128B (d=128) / 64B (d=64)
  * swizzled, the exact shared-memory image the tensor cores read.
  * Returns 0 or SAGE2_EINVAL. */
-#define SAGE2_WS_NREGIONS 15
+#define SAGE2_WS_NREGIONS 16
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 
 /* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */
@@ -136,7 +140,9 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
 /* Attention kernel only (Fig. 3 step 4), on a workspace filled by sage2_prepare with the same
- * shapes and flags. */
+ * shapes and flags.  The workspace is read only, except that the persistent v10 kernel
+ * (SAGE2_F_KERNEL_V10) uses the 256-byte sched region as its work counter and leaves it zeroed on
+ * exit: v10 calls on one workspace must not run concurrently on different streams. */
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
                     size_t ws_bytes, void* stream);
 

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsage2.so")
 SOURCES = ["sage2_api.cu"]
-DEPS = ["sage2_api.cu", "attn.cuh", "attn2.cuh", "attn4.cuh", "attn5.cuh", "attn6.cuh", "attn8.cuh", "dsg.cuh", "prep.cuh", "probe.cuh", "ptx.cuh"]
+DEPS = ["sage2_api.cu", "attn.cuh", "attn2.cuh", "attn4.cuh", "attn5.cuh", "attn6.cuh", "attn8.cuh", "attn10.cuh", "dsg.cuh", "prep.cuh", "probe.cuh", "ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

@@ -35,6 +35,7 @@ struct AttnParams {
     const float* vmean;     // [B*Hkv][D] V_m of the optional smooth V, or null
     const float* ds;        // Delta S * log2(e)/sqrt(d): [B*Hq][nT][N_pad], or triangular (ds_tri)
     int ds_tri;             // causal workspaces: row i of a head holds only keys < 128 (i + 1)
+    unsigned int* sched;    // v10 work-item counters [0] next item - grid, [1] finished CTAs (self-resetting)
     __half* out;            // [B][Hq][N][D]
     int32_t* s_dump;        // debug: [B*Hq][N_pad][N_pad] raw S_int (DUMP builds only)
     uint8_t* p_dump;        // debug: [B*Hq][N_pad][N_pad] P^ codes (DUMP builds only; may be null)

@@ -1,0 +1,483 @@
+// attn10.cuh -- SageAttention2 attention kernel v10 for sm_100a: v8 made PERSISTENT.
+// Same roles, arithmetic and TMEM plan as attn8.cuh (see there), but one CTA per SM loops over work
+// items (Q-block pair, h_q, b) in the v8 order (item w -> pair w % npairs, heaviest causal pairs
+// first within a head, then heads, then batches).  CTA c starts with item c; its producer thread takes
+// every further item from a global counter (p.sched[0], one atomicAdd per item, fetched one item
+// ahead), so faster SMs take more items and causal tails balance like the hardware block scheduler
+// would; the item index reaches the other roles through a 2-slot shared-memory ring published with
+// the Q barrier's arrive (release) and read after its wait (acquire).  The mbarrier
+// phases (K/V stage ring, per-tile S/P/R handshakes, Q) continue across items, so the next item's Q
+// and first K/V stages load while the current item drains, and barrier init / TMEM allocation / the
+// pipeline ramp happen once per SM instead of once per pair.  A q_empty barrier (one commit per MMA
+// issuer after its last MMA of an item) guards the Q^ tiles against the next item's load.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
+#include <cstdint>
+
+#include "attn.cuh"
+#include "attn2.cuh"
+#include "prep.cuh"
+#include "ptx.cuh"
+
+namespace sage2 {
+
+template <int D>
+struct Attn10Smem {
+    using B2 = Attn2Smem<D>;
+    static constexpr uint32_t TILE = B2::TILE;
+    static constexpr uint32_t Q0 = B2::Q0, Q1 = B2::Q1;
+    static constexpr uint32_t ST_K = B2::ST_K, ST_V = B2::ST_V, ST_DS0 = B2::ST_DS0, ST_DS1 = B2::ST_DS1,
+                              ST_DK = B2::ST_DK, STAGE = B2::STAGE, ST0 = B2::ST0;
+    static constexpr uint32_t P0 = B2::P0, P1 = B2::P1;
+    static constexpr uint32_t XM = P1 + 16384;              // float xm[2 tiles][2 buf][2 halves][128]
+    static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;  // float xl[2 tiles][2 halves][128]
+    static constexpr uint32_t BAR = XL + 2 * 2 * 128 * 4;
+    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 9;
+    static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
+    static constexpr uint32_t ITEM = TMEMPTR + 16;       // int item[2]: ring of published item indices
+    static constexpr uint32_t BYTES = ITEM + 16;
+    static constexpr uint32_t ALLOC = BYTES + 1024;
+};
+
+// GRAN: Q/K quantization granularity of the NEXT#4 ablation (0 per-thread = SageAttn2, 1 per-block,
+// 2 per-token; prep.cuh gran_nq / gran_nk give the stored scales per 128 tokens).
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
+__global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitems) {
+    using L = Attn10Smem<D>;
+    constexpr int DH = D / 2;                      // output channels per half
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
+
+    // warp index through a shuffle: provably warp-uniform, so everything derived from it (role,
+    // tile, half, TMEM / shared addresses) can live in uniform registers instead of being
+    // rematerialised from threadIdx every iteration under the softmax warps' register pressure
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+    const int wg = warp / 4;
+    const int nT = p.nT, Np = nT * 128;
+    const int npairs = (nT + 1) / 2;
+    struct Item {
+        int hq, b, bhq, bhk, it0, it1, nkv0, nkv1, nkv_max, ntiles;
+    };
+    auto item = [&](int w) {
+        Item t;
+        const int px = w % npairs, rest = w / npairs;
+        const int pair = CAUSAL ? (npairs - 1 - px) : px;   // heavy causal pairs first within a head
+        t.hq = rest % p.Hq;
+        t.b = rest / p.Hq;
+        t.bhq = t.b * p.Hq + t.hq;
+        t.bhk = t.b * p.Hkv + t.hq / (p.Hq / p.Hkv);
+        t.it0 = 2 * pair;
+        t.it1 = 2 * pair + 1;
+        t.nkv0 = CAUSAL ? t.it0 + 1 : nT;
+        t.nkv1 = (t.it1 < nT) ? (CAUSAL ? t.it1 + 1 : nT) : 0;
+        t.nkv_max = t.nkv0 > t.nkv1 ? t.nkv0 : t.nkv1;
+        t.ntiles = t.nkv1 > 0 ? 2 : 1;
+        return t;
+    };
+    auto s_as_float = [](uint32_t u) { return QKF8 ? __uint_as_float(u) : (float)(int32_t)u; };
+    auto s_as_int = [](uint32_t u) { return QKF8 ? (int32_t)__uint_as_float(u) : (int32_t)u; };
+    // TIMING builds: clock64 stamps (CTA (0,0,0); thread 0 of the half-0 warpgroup of each tile) ->
+    // (uint64*)p.s_dump [tile][j][slot]
+    const bool tsel = TIMING && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    auto ts = [&](int who, int j, int slot) {
+        if (TIMING && tsel && j < 64)
+            reinterpret_cast<unsigned long long*>(p.s_dump)[(who * 64 + j) * 16 + slot] = clock64();
+    };
+    const uint32_t bar0 = sbase + L::BAR;
+    const uint32_t bar_q = bar0;
+    auto bar_kv_full = [&](int s) { return bar0 + 8 * (1 + s); };
+    auto bar_kv_empty = [&](int s) { return bar0 + 8 * (1 + kStages2 + s); };
+    auto bar_s_full = [&](int k) { return bar0 + 8 * (1 + 2 * kStages2 + k); };
+    auto bar_p_full = [&](int k) { return bar0 + 8 * (3 + 2 * kStages2 + k); };
+    auto bar_r_full = [&](int k) { return bar0 + 8 * (5 + 2 * kStages2 + k); };
+    auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * kStages2 + k); };
+    const uint32_t bar_q_empty = bar0 + 8 * (9 + 2 * kStages2);
+    auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(bar_kv_full(s), 1);
+            mbar_init(bar_kv_empty(s), 2);      // one arrival per Q tile (MMA commit or bypass)
+        }
+        mbar_init(bar_q_empty, 2);              // one arrival per MMA issuer per item
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(bar_s_full(k), 1);
+            mbar_init(bar_p_full(k), 256);
+            mbar_init(bar_r_full(k), 1);
+            mbar_init(bar_s_free(k), 256);
+        }
+        fence_mbar_init();
+    }
+    // control warpgroup first (warps 0-3: producer, MMA issuers), softmax warpgroups 1-4 (measured
+    // +1.5% against the control warps at the highest ids: the issuer hand-offs wake up sooner)
+    constexpr int CW = 0, SW0 = 1;
+    if (warp == 4 * CW) tmem_alloc<512>(sbase + L::TMEMPTR);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sgen + L::TMEMPTR);
+
+    if (wg == CW) {
+        setmaxnreg_dec<32>();
+        if (warp == 4 * CW && lane == 0) {
+            // ===================== producer =====================
+            const size_t tile_bytes = (size_t)128 * D;
+            const uint64_t keep = policy_evict_last();
+            volatile int* slot = reinterpret_cast<volatile int*>(sgen + L::ITEM);
+            int g = 0;                                          // stages issued
+            int w = blockIdx.x;
+            for (int n_it = 0;; ++n_it) {
+                if (w >= nitems) {                              // publish the end of work
+                    if (n_it >= 1) mbar_wait(bar_q_empty, (n_it - 1) & 1);
+                    slot[n_it & 1] = w;
+                    mbar_arrive(bar_q);
+                    break;
+                }
+                const int wn = (int)atomicAdd(p.sched, 1u) + (int)gridDim.x;   // next item, fetched early
+                const Item I = item(w);
+                auto load_q = [&]() {
+                    if (n_it >= 1) mbar_wait(bar_q_empty, (n_it - 1) & 1);   // previous item's QKs done
+                    slot[n_it & 1] = w;
+                    mbar_arrive_expect_tx(bar_q, L::TILE * I.ntiles);
+                    bulk_g2s(sbase + L::Q0, p.qhat + ((size_t)I.bhq * nT + I.it0) * tile_bytes, L::TILE, bar_q);
+                    if (I.ntiles == 2)
+                        bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)I.bhq * nT + I.it1) * tile_bytes, L::TILE, bar_q);
+                };
+                if (n_it == 0) load_q();
+                for (int j = 0; j < I.nkv_max; ++j, ++g) {
+                    if (j == 1 && n_it > 0) load_q();      // after the first K/V stage of the item
+                    const int s = g % kStages2;
+                    if (g >= kStages2) mbar_wait(bar_kv_empty(s), ((g / kStages2) - 1) & 1);
+                    const uint32_t sa = stage_addr(s);
+                    const bool d0 = j < I.nkv0, d1 = j < I.nkv1;
+                    constexpr int NGK = gran_nk(GRAN);
+                    mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 4 * NGK + 512 * (d0 + d1));
+                    bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)I.bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                    bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)I.bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                    bulk_g2s(sa + L::ST_DK, p.dk + ((size_t)I.bhk * nT + j) * NGK, 4 * NGK, bar_kv_full(s));
+                    if (d0)
+                        bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, I.bhq, I.it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+                    if (d1)
+                        bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, I.bhq, I.it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+                }
+                if (n_it > 0 && I.nkv_max == 1) load_q();
+                w = wn;
+            }
+        } else if (warp == 4 * CW + 1 || warp == 4 * CW + 2) {
+            // ============ MMA issuer for Q tile k (whole warp converged, one elected lane issues) ============
+            const int k = warp - (4 * CW + 1);
+            constexpr uint32_t IDQK = QKF8 ? idesc_e4m3(128, 128) : idesc_i8(128, 128);
+            constexpr uint32_t IDPV = idesc_e4m3(128, D);
+            const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
+            const uint64_t pdesc = smem_desc<128>(sbase + (k ? L::P1 : L::P0));
+            const uint32_t tS = tmem + 128 * k;
+            const volatile int* slot = reinterpret_cast<const volatile int*>(sgen + L::ITEM);
+            int st = 0;                                         // stage ring position
+            uint32_t kvph = 0, tph = 0;                         // its phase, this tile's S/P/R phase
+            bool first = true;                                  // no R of a previous step to wait for
+            for (int n_it = 0;; ++n_it) {
+                mbar_wait(bar_q, n_it & 1);                     // Q^ of item n_it landed (or end of work)
+                const int w = slot[n_it & 1];
+                if (w >= nitems) break;
+                const Item I = item(w);
+                const int my_nkv = k ? I.nkv1 : I.nkv0;
+                for (int j = 0; j < I.nkv_max; ++j) {
+                    const int s = st;
+                    const uint32_t ph = kvph;
+                    if (++st == kStages2) {
+                        st = 0;
+                        kvph ^= 1u;
+                    }
+                    mbar_wait(bar_kv_full(s), ph);
+                    if (j >= my_nkv) {                 // this tile is done: release the stage for it
+                        if (lane == 0) mbar_arrive(bar_kv_empty(s));
+                        continue;
+                    }
+                    if (!first) mbar_wait(bar_s_free(k), tph ^ 1u);   // R_k of the previous step read
+                    first = false;
+                    tc_fence_after();
+                    const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K);
+#pragma unroll
+                    for (int kk = 0; kk < D / 32; ++kk) {
+                        if (QKF8) mma_f8f6f4_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                        else mma_i8_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                    }
+                    mma_commit_w(bar_s_full(k));
+                    mbar_wait(bar_p_full(k), tph);                      // softmax_k wrote P^_k
+                    tc_fence_after();
+                    const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                    mma_commit_w(bar_r_full(k));
+                    mma_commit_w(bar_kv_empty(s));
+                    tph ^= 1u;
+                }
+                // Q^_k no longer read once this issuer's MMAs of the item complete
+                if (my_nkv > 0) mma_commit_w(bar_q_empty);
+                else if (lane == 0) mbar_arrive(bar_q_empty);
+            }
+        }
+    } else {
+        setmaxnreg_inc<112>();      // pool = 96 x 640 (launch): 32 + 4 x 112 = 5 x 96 (inc blocks otherwise)
+        // ============ softmax (key half h) + two-level promotion + epilogue for Q tile k ============
+        const int k = (wg - SW0) >> 1, h = (wg - SW0) & 1;
+        auto turn_wait = [&]() { named_bar_sync(1 + k, 512); };
+        auto turn_pass = [&]() { named_bar_arrive(1 + (1 - k), 512); };
+        auto pair_sync = [&]() { named_bar_sync(3 + k, 256); };   // the two halves of tile k
+        if (k == 1) turn_pass();                    // tile 0 takes the first MUFU turn
+        // stage ring position / phase and this tile's S-R phase, carried across items incrementally
+        // (no per-step division of a runtime-offset counter)
+        int st = 0;
+        uint32_t kvph = 0, tph = 0;
+        const volatile int* slot = reinterpret_cast<const volatile int*>(sgen + L::ITEM);
+        for (int n_it = 0;; ++n_it) {
+        mbar_wait(bar_q, n_it & 1);                 // item n_it published (its Q^ landed) or end of work
+        const int w = slot[n_it & 1];
+        if (w >= nitems) break;
+        // only what the KV loop needs stays live (b, h_q, bhk are re-derived for the epilogue: every
+        // extra loop-carried value here cost the loop re-materialised warp/lane state, measured)
+        const Item I = item(w);
+        const int bhq = I.bhq, nkv_max = I.nkv_max;
+        const int my_nkv = k ? I.nkv1 : I.nkv0, my_it = k ? I.it1 : I.it0;
+        if (my_nkv > 0) {
+            const int wq = warp & 3;
+            const int row = 32 * wq + lane;
+            const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+            const uint32_t tS = tmem + 128 * k + lane_off + 64 * h;      // this half's S columns
+            const uint32_t tR = tmem + 128 * k + lane_off + DH * h;      // this half's R channels
+            const uint32_t tO = tmem + 256 + D * k + lane_off + DH * h;  // this half's O channels
+            const int grow = my_it * 128 + row;
+            const float dqr = p.dq[((size_t)bhq * nT + my_it) * gran_nq(GRAN) +
+                                   (GRAN == 2 ? row : GRAN == 1 ? 0 : 8 * (row / 32) + (row % 8))] * p.qk_scale_log2;
+            uint8_t* sP = sgen + (k ? L::P1 : L::P0);
+            float* xm = reinterpret_cast<float*>(sgen + L::XM) + k * 512;    // [buf][half][128]
+            float m = -INFINITY, l = 0.0f;
+            const bool tme = TIMING && h == 0 && row == 0;
+            auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
+            for (int j = 0; j < my_nkv; ++j) {
+                const int s = st;
+                tss(j, 0);
+                mbar_wait(bar_kv_full(s), kvph);                    // Delta S / delta_K landed
+                mbar_wait(bar_s_full(k), tph);
+                tc_fence_after();
+                tss(j, 1);
+                const uint32_t dss = stage_addr(s) + (k ? L::ST_DS1 : L::ST_DS0) + 256 * h;
+                const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK) +
+                                   (GRAN == 1 ? h : 4 * h);
+                const uint32_t dkv = stage_addr(s) + L::ST_DK + 256 * h;   // per-token delta_K of this half
+                float2 sc2[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float v = dqr * dks[GRAN == 1 ? 0 : g];
+                    sc2[g] = make_float2(v, v);
+                }
+                const float2 dq2 = make_float2(dqr, dqr);
+                float sv[64];
+                {
+                    uint32_t r0[32], r1[32];
+                    tmem_ld32(tS + 0, r0);
+                    tmem_ld32(tS + 32, r1);
+                    tmem_wait_ld();
+                    reg_dep32(r0);
+                    reg_dep32(r1);
+                    tss(j, 9);
+                    if (DUMP) {
+                        int32_t* dst = p.s_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h;
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            dst[c] = s_as_int(r0[c]);
+                            dst[32 + c] = s_as_int(r1[c]);
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < 64; c += 4) {
+                        const uint32_t* rr = c < 32 ? r0 : r1;
+                        const float4 d4 = lds128(dss + 4 * c);
+                        const int g = (c % 8) / 2;
+                        float2 sa2 = sc2[g], sb2 = sc2[g + 1];
+                        if (GRAN == 2) {                     // one delta_K per key column
+                            const float4 k4 = lds128(dkv + 4 * c);
+                            sa2 = fmul2(make_float2(k4.x, k4.y), dq2);
+                            sb2 = fmul2(make_float2(k4.z, k4.w), dq2);
+                        }
+                        const float2 a = ffma2(make_float2(s_as_float(rr[c % 32]), s_as_float(rr[c % 32 + 1])),
+                                               sa2, make_float2(d4.x, d4.y));
+                        const float2 bq = ffma2(make_float2(s_as_float(rr[c % 32 + 2]), s_as_float(rr[c % 32 + 3])),
+                                                sb2, make_float2(d4.z, d4.w));
+                        sv[c] = a.x;
+                        sv[c + 1] = a.y;
+                        sv[c + 2] = bq.x;
+                        sv[c + 3] = bq.y;
+                    }
+                }
+                tss(j, 2);
+                if ((CAUSAL && j == my_it) || (j * 128 + 128 > p.N)) {   // C-18
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        const int key = j * 128 + 64 * h + c;
+                        if (key >= p.N || (CAUSAL && key > grow)) sv[c] = -INFINITY;
+                    }
+                }
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < 64; c += 8) {
+                    mx[0] = fmax3(mx[0], sv[c], sv[c + 1]);
+                    mx[1] = fmax3(mx[1], sv[c + 2], sv[c + 3]);
+                    mx[2] = fmax3(mx[2], sv[c + 4], sv[c + 5]);
+                    mx[3] = fmax3(mx[3], sv[c + 6], sv[c + 7]);
+                }
+                // exact row max over both halves (C-10): exchange through shared memory
+                const float mh = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
+                float* xmb = xm + (j & 1) * 256;
+                xmb[h * 128 + row] = mh;
+                pair_sync();
+                const float m_new = fmax3(m, mh, xmb[(1 - h) * 128 + row]);
+                const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
+                const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
+                tss(j, 3);
+                turn_wait();
+                tss(j, 4);
+                const float2 negm = make_float2(-m_use, -m_use);
+                float2 rs2 = make_float2(0.f, 0.f), rs2b = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c0 + 4 * q;
+                        const float2 x01 = fadd2(make_float2(sv[c], sv[c + 1]), negm);
+                        const float2 x23 = fadd2(make_float2(sv[c + 2], sv[c + 3]), negm);
+                        const float2 p01 = make_float2(ex2_approx(x01.x), ex2_approx(x01.y));
+                        const float2 p23 = make_float2(ex2_approx(x23.x), ex2_approx(x23.y));
+                        rs2 = fadd2(rs2, p01);
+                        rs2b = fadd2(rs2b, p23);
+                        const uint32_t lo = __nv_cvt_float2_to_fp8x2(p01, __NV_SATFINITE, __NV_E4M3);
+                        const uint32_t hi = __nv_cvt_float2_to_fp8x2(p23, __NV_SATFINITE, __NV_E4M3);
+                        w[q] = lo | (hi << 16);
+                    }
+                    *reinterpret_cast<uint4*>(sP + swz_off<128>(row, 64 * h + c0)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    if (DUMP && p.p_dump)
+                        *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h + c0) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(bar_p_full(k));
+                tss(j, 5);
+                turn_pass();
+                l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
+                m = m_new;
+                // ---- two-level promotion O = alpha * O + R(j) ----
+                mbar_wait(bar_r_full(k), tph);
+                tc_fence_after();
+                tss(j, 6);
+                uint32_t r[DH];
+#pragma unroll
+                for (int c = 0; c < DH; c += 32) tmem_ld32(tR + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < DH; c += 32) reg_dep32(*reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+                tc_fence_before();
+                mbar_arrive(bar_s_free(k));                // R in registers: QK(j+1) may overwrite S/R
+                tss(j, 7);
+                if (TIMING && k == 0 && lane == 0) ts(4 + wq + 4 * h, j, 7);   // every warp's R read
+                const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+                for (int c0 = 0; c0 < DH; c0 += 32) {
+                    uint32_t o[32];
+                    if (j > 0) {
+                        tmem_ld32(tO + c0, o);
+                        tmem_wait_ld();
+                        reg_dep32(o);
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float2 v = ffma2(a2, make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])),
+                                                   make_float2(__uint_as_float(r[c0 + c]), __uint_as_float(r[c0 + c + 1])));
+                            o[c] = __float_as_uint(v.x);
+                            o[c + 1] = __float_as_uint(v.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) o[c] = r[c0 + c];
+                    }
+                    tmem_st32(tO + c0, o);
+                }
+                tmem_wait_st();
+                tss(j, 8);
+                tph ^= 1u;
+                if (++st == kStages2) {
+                    st = 0;
+                    kvph ^= 1u;
+                }
+            }
+            // ---- epilogue: O / (l_0 + l_1) / 448 * delta_V  (l carries the 448 factor) ----
+            float* xl = reinterpret_cast<float*>(sgen + L::XL) + k * 256;
+            xl[h * 128 + row] = l;
+            pair_sync();
+            const float inv_l = 1.0f / (xl[row] + xl[128 + row]);
+            const Item E = item(slot[n_it & 1]);        // volatile re-read: item n_it is still published
+            const int hq = E.hq, b = E.b, bhk = E.bhk;
+            const float* dvp = p.dv + (size_t)bhk * D + DH * h;
+            const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D + DH * h : nullptr;   // smooth V: O + V_m
+            __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D + DH * h;
+#pragma unroll
+            for (int c0 = 0; c0 < DH; c0 += 32) {
+                uint32_t o[32];
+                tmem_ld32(tO + c0, o);
+                tmem_wait_ld();
+                reg_dep32(o);
+                if (grow < p.N) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 8) {
+                        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c));
+                        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c + 4));
+                        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 m0 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c)) : z;
+                        const float4 m1 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c + 4)) : z;
+                        __half2 h0 = __floats2half2_rn(fmaf(__uint_as_float(o[c]) * inv_l, d0.x, m0.x),
+                                                       fmaf(__uint_as_float(o[c + 1]) * inv_l, d0.y, m0.y));
+                        __half2 h1 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 2]) * inv_l, d0.z, m0.z),
+                                                       fmaf(__uint_as_float(o[c + 3]) * inv_l, d0.w, m0.w));
+                        __half2 h2 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 4]) * inv_l, d1.x, m1.x),
+                                                       fmaf(__uint_as_float(o[c + 5]) * inv_l, d1.y, m1.y));
+                        __half2 h3 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 6]) * inv_l, d1.z, m1.z),
+                                                       fmaf(__uint_as_float(o[c + 7]) * inv_l, d1.w, m1.w));
+                        *reinterpret_cast<uint4*>(orow + c0 + c) =
+                            make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                       *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+                    }
+                }
+            }
+        }
+        for (int j = my_nkv; j < nkv_max; ++j) {    // keep the MUFU turn protocol balanced
+            turn_wait();
+            turn_pass();
+        }
+        for (int j = my_nkv; j < nkv_max; ++j) {    // stages of the other tile only
+            if (++st == kStages2) {
+                st = 0;
+                kvph ^= 1u;
+            }
+        }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4 * CW) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+    if (threadIdx.x == 0) {     // the last CTA out resets the counters for the next launch
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+            p.sched[0] = 0;
+            p.sched[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace sage2

@@ -16,6 +16,7 @@
 #include "attn5.cuh"
 #include "attn6.cuh"
 #include "attn8.cuh"
+#include "attn10.cuh"
 #include "prep.cuh"
 #include "dsg.cuh"
 #include "probe.cuh"
@@ -66,6 +67,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
     const size_t nT = (size_t)(N + 127) / 128, Np = nT * 128;
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
     const size_t sizes[SAGE2_WS_NREGIONS - 1] = {
+        256,                  // sched (v10 work counters; zeroed by prepare, self-resetting)
         BHk * d * 8,          // ksum
         BHk * d * 4,          // vmax
         BHk * d * 8,          // vsum (smooth V)
@@ -93,7 +95,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
     return L;
 }
 
-enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_QBT, R_DS, R_END };
+enum { R_SCHED, R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_QBT, R_DS, R_END };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -150,7 +152,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const int qk_max = (flags & SAGE2_F_INT8) ? 127 : 7;
     const int smooth_q = (flags & SAGE2_F_INT8) ? 0 : 1;   // SageAttn2-8b: no Q smoothing
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
-    if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return cuda_rc();
+    if (cudaMemsetAsync(ws + L.off[R_SCHED], 0, L.off[R_KBAR] - L.off[R_SCHED], st) != cudaSuccess) return cuda_rc();
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
     // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
@@ -286,6 +288,29 @@ int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+template <int D, bool CAUSAL, bool DUMP>
+int launch_attn10_t(const AttnParams& p, int B, cudaStream_t st) {
+    using L = Attn10Smem<D>;
+    constexpr uint32_t smem = L::ALLOC;
+    static bool configured = false;
+    static int nsm = 0;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k_attn10<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+            return cuda_rc();
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            return cuda_rc();
+        configured = true;
+    }
+    const long long nitems = (long long)((p.nT + 1) / 2) * p.Hq * B;
+    if (nitems > 0x7fffffff) return SAGE2_EINVAL;
+    const int grid = (int)(nitems < nsm ? nitems : nsm);   // persistent: one CTA per SM
+    k_attn10<D, CAUSAL, DUMP><<<grid, 640, smem, st>>>(p, (int)nitems);
+    return cuda_rc();
+}
+
 template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn5_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn5Smem<D>;
@@ -313,6 +338,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.dv = reinterpret_cast<const float*>(ws + L.off[R_DV]);
     p.vmean = (flags & SAGE2_F_SMOOTH_V) ? reinterpret_cast<const float*>(ws + L.off[R_VMEAN]) : nullptr;
     p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
+    p.sched = reinterpret_cast<unsigned int*>(const_cast<uint8_t*>(ws + L.off[R_SCHED]));   // v10 scratch (sage2.h)
     p.ds_tri = (flags & SAGE2_F_CAUSAL) ? 1 : 0;
     p.out = reinterpret_cast<__half*>(out);
     p.s_dump = s_dump;
@@ -354,7 +380,24 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
         return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
     }
-    // default: v8 (C2-32K: d=128 1212 vs 1059 TOPS for v6, causal 1190 vs 1023; d=64 658 vs 644)
+    if (flags & SAGE2_F_KERNEL_V10) {   // v10 -- persistent v8 (attn10.cuh)
+        if (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | SAGE2_F_DEBUG_TIMING))
+            return SAGE2_EINVAL;
+        if (s_dump) {
+            if (d == 64) return launch_attn10_t<64, false, true>(p, B, st);
+            return launch_attn10_t<128, false, true>(p, B, st);
+        }
+        if (d == 64) return causal ? launch_attn10_t<64, true, false>(p, B, st) : launch_attn10_t<64, false, false>(p, B, st);
+        return causal ? launch_attn10_t<128, true, false>(p, B, st) : launch_attn10_t<128, false, false>(p, B, st);
+    }
+    // default for d = 128, non-causal, N <= 8192: v10 (persistent v8; C2-1K 751 vs 718 TOPS, C2-4K
+    // 1134 vs 1101; from 16K on and for d = 64 / causal v8 is faster: DESIGN.md section 9)
+    constexpr int kAny = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
+                         SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V8 | SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA |
+                         SAGE2_F_DEBUG_TIMING | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
+    if (!(flags & kAny) && !s_dump && d == 128 && !causal && p.nT <= 64)
+        return launch_attn10_t<128, false, false>(p, B, st);
+    // default otherwise: v8 (C2-32K: d=128 1212 vs 1059 TOPS for v6, causal 1190 vs 1023; d=64 658 vs 644)
     if ((flags & SAGE2_F_KERNEL_V8) || !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1))) {
         // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
         const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;

@@ -14,8 +14,8 @@ LIB_PATH = os.environ.get("SAGE2_LIB") or os.path.join(_HERE, "libsage2.so")
 
 F_CAUSAL = 1
 F_INT8 = 2
-WS_NREGIONS = 15
-REGIONS = ("ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "qbt", "ds", "end")
+WS_NREGIONS = 16
+REGIONS = ("sched", "ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "qbt", "ds", "end")
 
 _lib = None
 
@@ -149,13 +149,13 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v6": 8192, "v8": 4096, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v10": 16384, "v6": 8192, "v8": 4096, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
               smooth_v=False, gran="thread"):
-    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default = v8 for d=128 and
-    v6 for d=64, or an A/B variant;
+    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default = v10 (persistent)
+    for d=128 non-causal N <= 8192, v8 otherwise; or an A/B variant;
     qk_e4m3 must match the prepare() call)."""
     _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
                                  flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],

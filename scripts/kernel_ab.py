@@ -25,7 +25,7 @@ out = torch.empty_like(q)
 L = sage2.lib()
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ops = 4.0 * B * H * N * N * d
-VARIANTS = [("default", 0), ("v6", 8192), ("v6_causal", 8193), ("v8", 4096), ("v8_causal", 4097), ("v8f8", 4096 + 2048),
+VARIANTS = [("default", 0), ("v10", 16384), ("v10_causal", 16385), ("v6", 8192), ("v6_causal", 8193), ("v8", 4096), ("v8_causal", 4097), ("v8f8", 4096 + 2048),
             ("v6f8", 8192 + 2048), ("v1", 128), ("v1_causal", 129), ("v5", 512), ("v5_causal", 513),
             ("v4", 8), ("v4_causal", 9), ("v0", 4), ("v4_nullsm", 24), ("v4_nullmma", 40), ("v1_nullmma", 160)]
 if len(sys.argv) > 3 and sys.argv[3]:

@@ -239,7 +239,7 @@ def test_accuracy_vs_fp32_attention():
         assert cs > min_cos, (kind, cs)
 
 
-@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v8", 128), ("v6", 128), ("v1", 128), ("v5", 64), ("v4", 128), ("v0", 128)])
+@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v10", 128), ("v8", 128), ("v6", 128), ("v1", 128), ("v5", 64), ("v4", 128), ("v0", 128)])
 @pytest.mark.parametrize("d,causal,N", [(128, False, 384), (64, True, 384), (128, True, 300), (64, False, 200)])
 def test_kernel_variants(kernel, kv_tile, d, causal, N):
     """Every attention-kernel variant kept for A/B timing matches the oracle run with its b_kv (C-9).
@@ -257,6 +257,26 @@ def test_kernel_variants(kernel, kv_tile, d, causal, N):
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
                                    OracleConfig(causal=causal, kv_tile=kv_tile), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(2, 40, 8, 600, 128, False), (2, 40, 8, 600, 128, True),
+                                                 (1, 64, 64, 1100, 64, True), (3, 30, 10, 1024, 128, False)])
+def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
+    """v10 (persistent: one CTA per SM looping over (pair, h_q, b) items, barrier phases carried across
+    items) with more items than SMs, so CTAs run 2-5 items each: bit-identical to v8 (same arithmetic,
+    different schedule) on the whole tensor, and the oracle on a sample of Q blocks spread over items."""
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=21)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d, causal=causal)
+    sage2.prepare(qg, kg, vg, ws, causal=causal)
+    o10, o8 = torch.empty_like(qg), torch.empty_like(qg)
+    sage2.attention(o10, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+    sage2.attention(o8, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v8")
+    torch.cuda.synchronize()
+    assert torch.equal(o10, o8), "v10 differs from v8"
+    nT = (N + 127) // 128
+    units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)][::11]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
+    _compare_out(to_np16(o10).astype(np.float64), res, units, N)
 
 
 @pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128)])
