@@ -309,13 +309,14 @@ def run_ours(args, world, rank, local):
         validation = {"collective": "all_gather (NCCL)", "gathered_bytes": int(out.numel() * 2 * world),
                       "gather_ms_wall": g_ms, "ranks_mismatched": bad,
                       "check": "rank 0 recomputes every rank's first unit alone: bitwise equal"}
+    kver = sage2.attention_kernel(N, d, causal=causal)
     line = {
         "metric": "attention TOPS (SageAttn2-4b forward)", "value": value, "unit": "TOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
         "data": "synthetic", "config": workload_config(name),
         "gpu_launches": 5 * args.steps,
-        "roofline": {"bound": "tensor", "kernel": "k_attn8 (tcgen05 attention, v8)", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": f"k_attn{kver} (tcgen05 attention, v{kver})", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms_max,
                      "kernel_share_of_step": kms_max / ms_max},

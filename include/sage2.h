@@ -143,6 +143,11 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
  * shapes and flags.  The workspace is read only, except that the persistent v10 kernel
  * (SAGE2_F_KERNEL_V10) uses the 256-byte sched region as its work counter and leaves it zeroed on
  * exit: v10 calls on one workspace must not run concurrently on different streams. */
+/* Which attention kernel sage2_attention runs for (N, d, flags): 10, 8, 6, 5, 4, 1 or 0 (the
+ * version numbers of the SAGE2_F_KERNEL_* selectors; with no selector: 10 for d = 128, non-causal,
+ * N <= 8192 without QK_E4M3 / GRAN flags, else 8).  Host-only, no CUDA call; never fails. */
+int sage2_attention_kernel(int N, int d, int flags);
+
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
                     size_t ws_bytes, void* stream);
 

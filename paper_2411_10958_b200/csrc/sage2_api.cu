@@ -327,6 +327,15 @@ int launch_attn5_t(const AttnParams& p, int B, cudaStream_t st) {
 }
 
 
+// the no-kernel-flag dispatch rule shared by launch_attention and sage2_attention_kernel
+bool default_is_v10(int flags, int N, int d) {
+    constexpr int kAny = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
+                         SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_DEBUG_NULLSM |
+                         SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK |
+                         SAGE2_F_GRAN_TOKEN;
+    return !(flags & kAny) && d == 128 && !(flags & SAGE2_F_CAUSAL) && (N + 127) / 128 <= 64;
+}
+
 int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
                      const Layout& L, cudaStream_t st) {
     AttnParams p;
@@ -392,11 +401,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     }
     // default for d = 128, non-causal, N <= 8192: v10 (persistent v8; C2-1K 751 vs 718 TOPS, C2-4K
     // 1134 vs 1101; from 16K on and for d = 64 / causal v8 is faster: DESIGN.md section 9)
-    constexpr int kAny = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
-                         SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V8 | SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA |
-                         SAGE2_F_DEBUG_TIMING | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
-    if (!(flags & kAny) && !s_dump && d == 128 && !causal && p.nT <= 64)
-        return launch_attn10_t<128, false, false>(p, B, st);
+    if (!s_dump && default_is_v10(flags, N, d)) return launch_attn10_t<128, false, false>(p, B, st);
     // default otherwise: v8 (C2-32K: d=128 1212 vs 1059 TOPS for v6, causal 1190 vs 1023; d=64 658 vs 644)
     if ((flags & SAGE2_F_KERNEL_V8) || !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1))) {
         // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
@@ -534,6 +539,17 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
     auto* hv = reinterpret_cast<const __half*>(v);
     return d == 64 ? launch_prepare<64>(hq, hk, hv, B, H_q, H_kv, N, flags, ws, L, st)
                    : launch_prepare<128>(hq, hk, hv, B, H_q, H_kv, N, flags, ws, L, st);
+}
+
+int sage2_attention_kernel(int N, int d, int flags) {
+    if (flags & SAGE2_F_KERNEL_V0) return 0;
+    if (flags & SAGE2_F_KERNEL_V4) return 4;
+    if (flags & SAGE2_F_KERNEL_V5) return 5;
+    if (flags & SAGE2_F_KERNEL_V10) return 10;
+    if (flags & SAGE2_F_KERNEL_V8) return 8;
+    if (flags & SAGE2_F_KERNEL_V6) return 6;
+    if (flags & SAGE2_F_KERNEL_V1) return 1;
+    return default_is_v10(flags, N, d) ? 10 : 8;
 }
 
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,

@@ -51,6 +51,8 @@ def lib():
         L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
         L.sage2_microbench.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
         L.sage2_microbench.restype = I
+        L.sage2_attention_kernel.argtypes = [I, I, I]
+        L.sage2_attention_kernel.restype = I
         for n in ("sage2_attn", "sage2_attn_ws", "sage2_attn_ex", "sage2_workspace_layout", "sage2_prepare",
                   "sage2_attention", "sage2_debug_qk_int32", "sage2_probe_accumulator", "sage2_bench_mma",
                   "sage2_attn_host"):
@@ -161,6 +163,11 @@ def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel
                                  flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
     return out
+
+
+def attention_kernel(N, d, causal=False, kernel="default", qk_e4m3=False, gran="thread"):
+    """Version number of the attention kernel sage2_attention runs for these arguments (host only)."""
+    return int(lib().sage2_attention_kernel(N, d, flags(causal, False, qk_e4m3, False, gran) | KERNEL_FLAGS[kernel]))
 
 
 def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False):

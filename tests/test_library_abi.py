@@ -46,3 +46,16 @@ def test_no_cpu_fallback_without_gpu():
     except (ValueError, sage2.Sage2Error):
         return
     raise AssertionError("attn on CPU tensors must raise (no CPU fallback)")
+
+
+def test_default_kernel_dispatch_rule():
+    """Host-only query of the kernel sage2_attention runs (include/sage2.h sage2_attention_kernel):
+    v10 (persistent) only for d = 128, non-causal, N <= 8192 with no carrier / granularity flag."""
+    from paper_2411_10958_b200 import sage2
+    ak = sage2.attention_kernel
+    assert ak(4096, 128) == 10 and ak(8192, 128) == 10 and ak(200, 128) == 10
+    assert ak(8193, 128) == 8 and ak(32768, 128) == 8
+    assert ak(4096, 128, causal=True) == 8 and ak(4096, 64) == 8
+    assert ak(4096, 128, qk_e4m3=True) == 8 and ak(4096, 128, gran="block") == 8
+    assert ak(32768, 128, kernel="v10") == 10 and ak(1024, 128, kernel="v8") == 8
+    assert ak(1024, 64, kernel="v6") == 6 and ak(1024, 64, kernel="v0") == 0
