@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <vector>
 #include <cstring>
 #include <mutex>
 
@@ -619,9 +620,26 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q_host || !k_host || !v_host || !out_host) return SAGE2_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int grp = H_q / H_kv, units = B * H_kv;
-    int nch = units < 16 ? units : 16;
-    const int U = (units + nch - 1) / nch;                 // units per chunk
-    nch = (units + U - 1) / U;
+    const int nch0 = units < 16 ? units : 16;
+    const int U = (units + nch0 - 1) / nch0;               // units per full chunk
+    // chunk sizes: 1, 2, 4, ... < U, then full chunks, then ... 4, 2, 1 -- the first H2D and the
+    // last kernels + D2H are the parts the pipeline cannot overlap, so they are kept small
+    std::vector<int> ramp, csz;
+    int ramp_sum = 0;
+    for (int s = 1; s < U; s *= 2) {
+        ramp.push_back(s);
+        ramp_sum += s;
+    }
+    if (units >= 2 * ramp_sum + U) {
+        csz = ramp;
+        const int mid = units - 2 * ramp_sum;
+        for (int k = 0; k < mid / U; ++k) csz.push_back(U);
+        if (mid % U) csz.push_back(mid % U);
+        csz.insert(csz.end(), ramp.rbegin(), ramp.rend());
+    } else {
+        for (int u = 0; u < units; u += U) csz.push_back(units - u < U ? units - u : U);
+    }
+    const int nch = (int)csz.size();
     const size_t qu = (size_t)grp * N * d * 2, ku = (size_t)N * d * 2;   // bytes per unit
     const size_t wsb = sage2_workspace_bytes(1, U * grp, U, N, d, causal);
     // three streams / buffer sets in flight: chunk c's kernels, chunk c+1's H2D and chunk c-1's D2H
@@ -649,8 +667,8 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
     for (int i = 0; i < nbuf && rc == SAGE2_OK; ++i)
         if (cudaStreamWaitEvent(ss[i], ev_start, 0) != cudaSuccess) bad();   // allocations are ready
     const int flags = causal ? SAGE2_F_CAUSAL : 0;
-    for (int c = 0; c < nch && rc == SAGE2_OK; ++c) {
-        const int i = c % NB, u0 = c * U, nu = (units - u0) < U ? (units - u0) : U;
+    for (int c = 0, u0 = 0; c < nch && rc == SAGE2_OK; u0 += csz[c], ++c) {
+        const int i = c % NB, nu = csz[c];
         cudaStream_t s = ss[i];
         const char* qh = static_cast<const char*>(q_host) + (size_t)u0 * qu;
         const char* kh = static_cast<const char*>(k_host) + (size_t)u0 * ku;

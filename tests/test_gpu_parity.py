@@ -197,10 +197,13 @@ def test_deterministic():
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(2, 8, 4, 300, 64, True), (3, 12, 3, 513, 128, False),
-                                                 (1, 20, 20, 256, 128, True)])
+                                                 (1, 20, 20, 256, 128, True), (2, 35, 35, 200, 64, False),
+                                                 (4, 64, 32, 130, 128, True)])
 def test_host_entry_point_pipelined_chunks(B, Hq, Hkv, N, d, causal):
-    """sage2_attn_host splits the (b, h_kv) units into up to 8 chunks on two streams (ragged last
-    chunk for 9 and 20 units); the result is bitwise the one-shot device result."""
+    """sage2_attn_host splits the (b, h_kv) units into chunks on three streams: U = ceil(units/16)
+    units per full chunk, ramped 1, 2, 4, .. < U at both ends when there are enough units (20 units:
+    1, 2 x 9, 1; 70: 1, 2, 4, 5 x 11, 1, 4, 2, 1 (ragged middle); 128: 1, 2, 4, 8 x 14, 2, 4, 2, 1);
+    the result is bitwise the one-shot device result."""
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=8)
     od = sage2.attn(qg, kg, vg, causal=causal)
     oh = torch.empty_like(q).pin_memory()
