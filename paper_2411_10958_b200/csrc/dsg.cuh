@@ -9,9 +9,10 @@
 // fp32 accumulation in TMEM.  Error <= ~2^-20 * sum_c |q_bar_c||K'_tc| -- inside the parity bound
 // of DESIGN.md §5 (2e-6 * the same sum) and far inside the C-21 ambiguity margin.
 //
-// Roles (320 threads, one CTA per SM, persistent over work items (head, key tile, 256-block chunk)):
-//   warps 0-3   A producers: thread = key row; K' = fp32(K - k_bar) split into big/small and
-//               written as K-major SW128 tf32 slices (32 channels = one 128-byte atom per stage)
+// Roles (448 threads, one CTA per SM, persistent over work items (head, key tile, 256-block chunk)):
+//   warps 0-3, 10-13  A producers (two groups, alternate atoms): thread = key row; K' = fp32(K - k_bar)
+//               split into big/small and written as K-major SW128 tf32 slices (32 channels = one
+//               128-byte atom per stage)
 //   warps 4-7   epilogue: TMEM -> fp32 * log2(e)/sqrt(d) -> ds[bhq][i][t] (coalesced along t)
 //   warp 8      TMEM allocation + MMA issuer (tcgen05.mma.kind::tf32, M = 128 keys, N <= 256)
 //   warp 9      B loader: bulk-async copy of the pre-split q_bar slices written by k_q_quant
@@ -43,7 +44,7 @@ struct DsgSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict__ K, const float* __restrict__ kbar,
+__global__ void __launch_bounds__(448, 1) k_delta_s_tc(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                        const uint8_t* __restrict__ qbt, int N, int Hq, int Hkv,
                                                        int BHq, float scale_log2, float* __restrict__ ds, int tri) {
     // tri (causal workspaces): only query blocks i >= kt see key tile kt; rows are stored in the
@@ -97,10 +98,16 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
         return !tri || c * kDsgChunk + chunk_rows(c) - 1 >= kt;
     };
 
-    if (warp < 4) {
+    if (warp < 4 || warp >= 10) {
         // ===================== A producers: K' = fp32(K - k_bar) -> tf32 big/small =====================
-        const int t = threadIdx.x;
-        uint32_t g = 0;
+        // two groups of 128 threads (warps 0-3 and 10-13), thread = key row: group pg writes the atoms
+        // a = pg, pg + 2, .. and therefore always stage pg (NA is even, so the global atom counter has
+        // the parity of a).  One group alone was latency-bound (one dependent chain per SM
+        // sub-partition): C2-4K 142 us, C2-32K 1.59 ms for this kernel.
+        const int pg = warp >= 10 ? 1 : 0;
+        const int t = threadIdx.x - (pg ? 320 : 0);
+        constexpr int NAG = NA / 2;                        // atoms per group
+        uint32_t it = 0;                                   // live items done by this CTA
         for (int w = blockIdx.x; w < items; w += gridDim.x) {
             if (!live(w)) continue;
             int bhq, kt, c;
@@ -108,24 +115,35 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
             const int b = bhq / Hq, hk = (bhq % Hq) / (Hq / Hkv), bhk = b * Hkv + hk;
             const int key = kt * 128 + t;
             const float* kb = kbar + (size_t)bhk * D;
-            uint4 raw[D / 8];
+            uint4 raw[NAG * 4];                            // this group's channels of the key row
 #pragma unroll
-            for (int j = 0; j < D / 8; ++j)
-                raw[j] = key < N ? __ldg(reinterpret_cast<const uint4*>(K + ((size_t)bhk * N + key) * D) + j)
-                                 : make_uint4(0, 0, 0, 0);
+            for (int ai = 0; ai < NAG; ++ai)
 #pragma unroll
-            for (int a = 0; a < NA; ++a, ++g) {
-                const int s = g & 1;
+                for (int jj = 0; jj < 4; ++jj)
+                    raw[ai * 4 + jj] =
+                        key < N ? __ldg(reinterpret_cast<const uint4*>(K + ((size_t)bhk * N + key) * D) +
+                                        (2 * ai + pg) * 4 + jj)
+                                : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int ai = 0; ai < NAG; ++ai) {
+                const int a = 2 * ai + pg;
+                const uint32_t g = it * NA + a;            // the MMA issuer's atom counter
+                const int s = pg;
                 if (g >= 2) mbar_wait(st_empty(s), ((g >> 1) - 1) & 1);
                 const uint32_t sa = stage(s);
+                // this atom's 32 k_bar channels up front (vector loads): the shared stores below are
+                // asm with a memory clobber, so per-channel loads would each wait out their latency
+                float4 kb4[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) kb4[q] = __ldg(reinterpret_cast<const float4*>(kb + a * 32) + q);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {              // 16-byte chunk = 4 channels
-                    const int c0 = a * 32 + q * 4;
-                    const __half* h = reinterpret_cast<const __half*>(&raw[c0 / 8]) + (c0 % 8);
+                    const __half* h = reinterpret_cast<const __half*>(&raw[ai * 4 + q / 2]) + (q % 2) * 4;
+                    const float kbq[4] = {kb4[q].x, kb4[q].y, kb4[q].z, kb4[q].w};
                     float big[4], sml[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float kp = key < N ? __fsub_rn(__half2float(h[e]), __ldg(kb + c0 + e)) : 0.0f;   // O-2
+                        const float kp = key < N ? __fsub_rn(__half2float(h[e]), kbq[e]) : 0.0f;   // O-2
                         big[e] = tf32_big(kp);
                         sml[e] = __fsub_rn(kp, big[e]);
                     }
@@ -138,6 +156,7 @@ __global__ void __launch_bounds__(320, 1) k_delta_s_tc(const __half* __restrict_
                 fence_proxy_async_smem();                  // generic-proxy stores -> tcgen05.mma reads
                 mbar_arrive(a_full(s));
             }
+            ++it;
         }
     } else if (warp < 8) {
         // ===================== epilogue =====================

@@ -205,7 +205,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     }
     const long long items = (long long)BHq * nT * ((nT + 255) / 256);
     const int grid = (int)std::min<long long>(items, nsm);
-    k_delta_s_tc<D><<<grid, 320, DsgSmem<D>::ALLOC, st>>>(
+    k_delta_s_tc<D><<<grid, 448, DsgSmem<D>::ALLOC, st>>>(
         k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]), ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2,
         reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
     return cuda_rc();

@@ -276,6 +276,13 @@ def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
     sage2.attention(o8, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v8")
     torch.cuda.synchronize()
     assert torch.equal(o10, o8), "v10 differs from v8"
+    # the work counter resets itself at the end of a launch: a second launch on the same workspace
+    # (no prepare in between) must cover every item again
+    o10b = torch.full_like(qg, float("nan"))
+    sage2.attention(o10b, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+    torch.cuda.synchronize()
+    assert torch.equal(o10b, o8), "second v10 launch differs (work counter not reset)"
+    assert int(ws[sage2.layout(B, Hq, Hkv, N, d)["sched"]:][:8].view(torch.int32).abs().sum()) == 0
     nT = (N + 127) // 128
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)][::11]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
