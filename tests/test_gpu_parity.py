@@ -477,3 +477,46 @@ def test_delta_s_tensor_core_path(causal):
             got = ds[off:off + keys].astype(np.float64) / (LOG2E / math.sqrt(d))
             bound = 2e-6 * (np.abs(kv["kprime"][:keys]).astype(np.float64) @ np.abs(qb["qbar"]).astype(np.float64))
             assert np.all(np.abs(got - ref[:keys]) <= bound + 1e-6 * np.abs(ref[:keys]) + 1e-30)
+
+
+def _near_midpoint_v(N, d, seed):
+    """V [N, d] fp16 whose quotients V / delta_V (IEEE fp32, delta_V = absmax / 448 as the oracle
+    computes it) sit within 6 fp32 ulps of an E4M3 rounding midpoint, plus E4M3-subnormal and
+    exactly-representable quotients: the cases the kernel's reciprocal fast path must hand to IEEE
+    division (prep.cuh v_near_midpoint)."""
+    rng = np.random.default_rng(seed)
+    allpos = np.arange(0x0001, 0x7C00, dtype=np.uint16).view(np.float16)          # finite positive fp16
+    v = np.zeros((N, d), np.float16)
+    for c in range(d):
+        m = np.float16(rng.uniform(0.5, 40.0))
+        delta = np.float32(np.float32(m) / np.float32(448.0))
+        ys = allpos[allpos.astype(np.float32) <= np.float32(m)]
+        qs = (ys.astype(np.float32) / delta).astype(np.float32)
+        b = qs.view(np.uint32)
+        low = (b & 0xFFFFF).astype(np.int64)
+        hard = (np.abs(low - 0x80000) <= 6) & (b >= 0x3C800000)
+        sub = b < 0x3C800000
+        exact = low == 0
+        pick = np.concatenate([rng.permutation(np.flatnonzero(hard))[: (N - 1) // 2],
+                               rng.permutation(np.flatnonzero(sub))[: (N - 1) // 4],
+                               rng.permutation(np.flatnonzero(exact))[: (N - 1) // 8]])
+        col = ys[rng.choice(pick, N - 1)] * rng.choice(np.array([-1, 1], np.float16), N - 1)
+        v[0, c] = m
+        v[1:, c] = rng.permutation(col)
+    return v
+
+
+@pytest.mark.parametrize("N,d", [(2048, 64), (1000, 128)])
+def test_v_codes_near_e4m3_midpoints(N, d):
+    """V codes stay bit-exact with the oracle's IEEE-division quantizer (C-6) on inputs built so most
+    quotients are within a few ulps of an E4M3 rounding midpoint or in the E4M3 subnormal range."""
+    B, Hq, Hkv = 1, 1, 1
+    q, k, _, qg, kg, _ = _inputs(B, Hq, Hkv, N, d, "iid", seed=4)
+    v = torch.from_numpy(_near_midpoint_v(N, d, seed=5)).view(1, 1, N, d)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, v.cuda(), ws)
+    torch.cuda.synchronize()
+    g = read_prepared(ws, sage2.layout(B, Hq, Hkv, N, d), B, Hq, Hkv, N, d)
+    kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
+    assert np.array_equal(g["dv"][0].view(np.uint32), kv["dv"].view(np.uint32))
+    assert np.array_equal(g["vhat"][0], kv["vhat"])
