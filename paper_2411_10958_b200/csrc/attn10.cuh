@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
     const int nT = p.nT, Np = nT * 128;
     const int npairs = (nT + 1) / 2;
     struct Item {
-        int hq, b, bhq, bhk, it0, it1, nkv0, nkv1, nkv_max, ntiles;
+        int hq, b, bhq, bhk, it0, it1, nkv0, nkv1, nkv_max, npad, ntiles;
     };
     auto item = [&](int w) {
         Item t;
@@ -73,6 +73,10 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
         t.nkv0 = CAUSAL ? t.it0 + 1 : nT;
         t.nkv1 = (t.it1 < nT) ? (CAUSAL ? t.it1 + 1 : nT) : 0;
         t.nkv_max = t.nkv0 > t.nkv1 ? t.nkv0 : t.nkv1;
+        // stages an item occupies: padded to a multiple of the ring depth, so every item starts at
+        // ring position 0 with one phase bit for all stages (the softmax loop then derives stage
+        // and phase from its uniform step counter, as in v8)
+        t.npad = (t.nkv_max + kStages2 - 1) / kStages2 * kStages2;
         t.ntiles = t.nkv1 > 0 ? 2 : 1;
         return t;
     };
@@ -147,10 +151,14 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                         bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)I.bhq * nT + I.it1) * tile_bytes, L::TILE, bar_q);
                 };
                 if (n_it == 0) load_q();
-                for (int j = 0; j < I.nkv_max; ++j, ++g) {
+                for (int j = 0; j < I.npad; ++j, ++g) {
                     if (j == 1 && n_it > 0) load_q();      // after the first K/V stage of the item
                     const int s = g % kStages2;
                     if (g >= kStages2) mbar_wait(bar_kv_empty(s), ((g / kStages2) - 1) & 1);
+                    if (j >= I.nkv_max) {                  // padding stage: completes with no data
+                        mbar_arrive(bar_kv_full(s));
+                        continue;
+                    }
                     const uint32_t sa = stage_addr(s);
                     const bool d0 = j < I.nkv0, d1 = j < I.nkv1;
                     constexpr int NGK = gran_nk(GRAN);
@@ -163,7 +171,6 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                     if (d1)
                         bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, I.bhq, I.it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
                 }
-                if (n_it > 0 && I.nkv_max == 1) load_q();
                 w = wn;
             }
         } else if (warp == 4 * CW + 1 || warp == 4 * CW + 2) {
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                 if (w >= nitems) break;
                 const Item I = item(w);
                 const int my_nkv = k ? I.nkv1 : I.nkv0;
-                for (int j = 0; j < I.nkv_max; ++j) {
+                for (int j = 0; j < I.npad; ++j) {
                     const int s = st;
                     const uint32_t ph = kvph;
                     if (++st == kStages2) {
@@ -230,17 +237,16 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
         if (k == 1) turn_pass();                    // tile 0 takes the first MUFU turn
         // stage ring position / phase and this tile's S-R phase, carried across items incrementally
         // (no per-step division of a runtime-offset counter)
-        int st = 0;
-        uint32_t kvph = 0, tph = 0;
+        uint32_t pb = 0, tb = 0;     // item-start phase of every ring stage / of this tile's S-P-R
         const volatile int* slot = reinterpret_cast<const volatile int*>(sgen + L::ITEM);
         for (int n_it = 0;; ++n_it) {
         mbar_wait(bar_q, n_it & 1);                 // item n_it published (its Q^ landed) or end of work
-        const int w = slot[n_it & 1];
+        const int w = __shfl_sync(0xffffffffu, slot[n_it & 1], 0);   // provably warp-uniform
         if (w >= nitems) break;
         // only what the KV loop needs stays live (b, h_q, bhk are re-derived for the epilogue: every
         // extra loop-carried value here cost the loop re-materialised warp/lane state, measured)
         const Item I = item(w);
-        const int bhq = I.bhq, nkv_max = I.nkv_max;
+        const int bhq = I.bhq, nkv_max = I.nkv_max, npad = I.npad;
         const int my_nkv = k ? I.nkv1 : I.nkv0, my_it = k ? I.it1 : I.it0;
         if (my_nkv > 0) {
             const int wq = warp & 3;
@@ -258,7 +264,8 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
             const bool tme = TIMING && h == 0 && row == 0;
             auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
             for (int j = 0; j < my_nkv; ++j) {
-                const int s = st;
+                const int s = j % kStages2;
+                const uint32_t kvph = pb ^ ((uint32_t)(j / kStages2) & 1u), tph = tb ^ ((uint32_t)j & 1u);
                 tss(j, 0);
                 mbar_wait(bar_kv_full(s), kvph);                    // Delta S / delta_K landed
                 mbar_wait(bar_s_full(k), tph);
@@ -407,18 +414,13 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                 }
                 tmem_wait_st();
                 tss(j, 8);
-                tph ^= 1u;
-                if (++st == kStages2) {
-                    st = 0;
-                    kvph ^= 1u;
-                }
             }
             // ---- epilogue: O / (l_0 + l_1) / 448 * delta_V  (l carries the 448 factor) ----
             float* xl = reinterpret_cast<float*>(sgen + L::XL) + k * 256;
             xl[h * 128 + row] = l;
             pair_sync();
             const float inv_l = 1.0f / (xl[row] + xl[128 + row]);
-            const Item E = item(slot[n_it & 1]);        // volatile re-read: item n_it is still published
+            const Item E = item(__shfl_sync(0xffffffffu, slot[n_it & 1], 0));        // volatile re-read: item n_it is still published
             const int hq = E.hq, b = E.b, bhk = E.bhk;
             const float* dvp = p.dv + (size_t)bhk * D + DH * h;
             const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D + DH * h : nullptr;   // smooth V: O + V_m
@@ -456,12 +458,8 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
             turn_wait();
             turn_pass();
         }
-        for (int j = my_nkv; j < nkv_max; ++j) {    // stages of the other tile only
-            if (++st == kStages2) {
-                st = 0;
-                kvph ^= 1u;
-            }
-        }
+        pb ^= (uint32_t)(npad / kStages2) & 1u;
+        tb ^= (uint32_t)my_nkv & 1u;
         }
     }
     tc_fence_before();
