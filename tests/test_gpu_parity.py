@@ -289,6 +289,22 @@ def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
     _compare_out(to_np16(o10).astype(np.float64), res, units, N)
 
 
+@pytest.mark.parametrize("int8,smooth_v", [(True, False), (False, True), (True, True)])
+def test_persistent_v10_variants_match_v8(int8, smooth_v):
+    """SageAttn2-8b and smooth V through v10 with more items than SMs (B*H_q*pairs = 2*48*3 = 288):
+    bitwise the v8 output (same arithmetic, persistent schedule)."""
+    B, Hq, Hkv, N, d = 2, 48, 16, 700, 128
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=31)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws, int8=int8, smooth_v=smooth_v)
+    o10, o8 = torch.empty_like(qg), torch.empty_like(qg)
+    sage2.attention(o10, ws, B, Hq, Hkv, N, d, int8=int8, smooth_v=smooth_v, kernel="v10")
+    sage2.attention(o8, ws, B, Hq, Hkv, N, d, int8=int8, smooth_v=smooth_v, kernel="v8")
+    torch.cuda.synchronize()
+    assert torch.equal(o10, o8)
+    assert sage2.attention_kernel(N, d) == 10     # and this shape's default is v10
+
+
 @pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128)])
 def test_qk_e4m3_carrier_s_bit_exact(N, d):
     """E4M3-carrier QK^T (SAGE2_F_QK_E4M3): the fp32 accumulator of kind::f8f6f4 over E4M3-coded
