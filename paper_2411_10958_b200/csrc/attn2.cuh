@@ -32,7 +32,10 @@
 
 namespace sage2 {
 
-constexpr int kStages2 = 3;
+#ifndef SAGE2_KSTAGES
+#define SAGE2_KSTAGES 3
+#endif
+constexpr int kStages2 = SAGE2_KSTAGES;   // K/V ring depth (A/B builds: -DSAGE2_KSTAGES=4)
 
 template <int D>
 struct Attn2Smem {
