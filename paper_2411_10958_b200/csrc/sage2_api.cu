@@ -289,14 +289,14 @@ int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP>
+template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn10_t(const AttnParams& p, int B, cudaStream_t st) {
     using L = Attn10Smem<D>;
     constexpr uint32_t smem = L::ALLOC;
     static bool configured = false;
     static int nsm = 0;
     if (!configured) {
-        if (cudaFuncSetAttribute(k_attn10<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        if (cudaFuncSetAttribute(k_attn10<D, CAUSAL, DUMP, false, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
             cudaSuccess)
             return cuda_rc();
         int dev = 0;
@@ -308,7 +308,7 @@ int launch_attn10_t(const AttnParams& p, int B, cudaStream_t st) {
     const long long nitems = (long long)((p.nT + 1) / 2) * p.Hq * B;
     if (nitems > 0x7fffffff) return SAGE2_EINVAL;
     const int grid = (int)(nitems < nsm ? nitems : nsm);   // persistent: one CTA per SM
-    k_attn10<D, CAUSAL, DUMP><<<grid, 640, smem, st>>>(p, (int)nitems);
+    k_attn10<D, CAUSAL, DUMP, false, TIMING><<<grid, 640, smem, st>>>(p, (int)nitems);
     return cuda_rc();
 }
 
@@ -391,8 +391,11 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
         return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
     }
     if (flags & SAGE2_F_KERNEL_V10) {   // v10 -- persistent v8 (attn10.cuh)
-        if (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | SAGE2_F_DEBUG_TIMING))
-            return SAGE2_EINVAL;
+        if (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) return SAGE2_EINVAL;
+        if (flags & SAGE2_F_DEBUG_TIMING) {   // softmax phase stamps of CTA 0 (its last item)
+            if (d == 64) return launch_attn10_t<64, false, false, true>(p, B, st);
+            return launch_attn10_t<128, false, false, true>(p, B, st);
+        }
         if (s_dump) {
             if (d == 64) return launch_attn10_t<64, false, true>(p, B, st);
             return launch_attn10_t<128, false, true>(p, B, st);
