@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
             uint8_t* sP = sgen + (k ? L::P1 : L::P0);
             float* xm = reinterpret_cast<float*>(sgen + L::XM) + k * 512;    // [buf][half][128]
             float m = -INFINITY, l = 0.0f;
-            const bool tme = TIMING && h == 0 && row == 0;
-            auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
+            const bool tme = TIMING && row == 0;           // thread 0 of each key half
+            auto tss = [&](int j, int slot) { if (tme) ts(h ? 2 + k : k, j, slot); };   // half 1 -> rows 2, 3
             for (int j = 0; j < my_nkv; ++j) {
                 const int s = j % kStages2;
                 const uint32_t kvph = pb ^ ((uint32_t)(j / kStages2) & 1u), tph = tb ^ ((uint32_t)j & 1u);

@@ -37,6 +37,12 @@ for j in range(8, 12):
         s = t[kk, j]
         print(f"  sm{kk}: start {s[0] - b:6d} Sready {s[1] - b:6d} Sld {s[9] - b:6d} deq {s[2] - b:6d} max {s[3] - b:6d} "
               f"turn {s[4] - b:6d} P {s[5] - b:6d} Rready {s[6] - b:6d} Rread {s[7] - b:6d} prom {s[8] - b:6d}")
+        if os.environ.get("V10"):            # v10: rows 2, 3 hold the key-half-1 softmax stamps
+            s1 = t[2 + kk, j]
+            print(f"  h1 {kk}: start {s1[0] - b:6d} Sready {s1[1] - b:6d} Sld {s1[9] - b:6d} deq {s1[2] - b:6d} "
+                  f"max {s1[3] - b:6d} turn {s1[4] - b:6d} P {s1[5] - b:6d} Rready {s1[6] - b:6d} "
+                  f"Rread {s1[7] - b:6d} prom {s1[8] - b:6d}")
+            continue
         m = t[2 + kk, j]
         m1 = t[2 + kk, j + 1]
         print(f"  mma{kk}: kvfull {m[0] - b:6d} sfree {m[1] - b:6d} QK {m[2] - b:6d} Pseen {m[3] - b:6d} PV {m[4] - b:6d} "
