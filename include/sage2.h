@@ -20,11 +20,12 @@
  *
  * Layouts (all contiguous, row-major):
  *   q   [B, H_q,  N, d] fp16      k, v [B, H_kv, N, d] fp16      out [B, H_q, N, d] fp16
- * d in {64, 128}; N >= 1 (ragged N allowed); H_q % H_kv == 0.
+ * d in {64, 128}; 1 <= N <= 2^22 (ragged N allowed); H_q % H_kv == 0; B * H_q <= 65535.
  *
  * Ownership: every pointer is caller-owned.  Device pointers must be 16-byte aligned device
- * memory of the current CUDA device.  The library never frees caller memory and keeps no state
- * between calls except cached kernel attributes.
+ * memory of the current CUDA device (workspaces 256-byte aligned).  The library never frees caller
+ * memory; between calls it keeps only cached kernel attributes (per device) and its stream-ordered
+ * memory pool (see sage2_attn, sage2_release_memory).
  *
  * Errors: functions return SAGE2_OK (0) or a negative code; nothing is printed and no C++
  * exception crosses the ABI.  Work is enqueued asynchronously on `stream` (a cudaStream_t, NULL =
@@ -48,36 +49,28 @@ extern "C" {
 #define SAGE2_ENOMEM (-3)       /* stream-ordered workspace allocation failed                    */
 #define SAGE2_ECUDA (-4)        /* a CUDA launch / API call failed (cudaGetLastError)            */
 
-/* Variant flags (bitwise OR) for the *_ex entry points. */
-#define SAGE2_F_CAUSAL 1   /* key <= query mask                                                  */
-#define SAGE2_F_INT8 2     /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing,  */
-                           /* P:70, P:476 (Table 3)                                    */
-#define SAGE2_F_KERNEL_V0 4 /* use the simple one-Q-tile-per-CTA attention kernel (A/B checks)  */
-/* Kernel variants (A/B timing and parity).  Default: v8 (csrc/attn8.cuh), b_kv = 128.            */
-#define SAGE2_F_KERNEL_V4 8 /* use the experimental v4 kernel (one Q tile / CTA, column-split     */
-                            /* softmax warpgroups, triple-buffered S/R in TMEM)                    */
-#define SAGE2_F_DEBUG_NULLSM 16 /* v4 timing experiment: skip softmax work (output is NOT attention)*/
-#define SAGE2_F_DEBUG_NULLMMA 32 /* v4 timing experiment: skip the MMAs (output is NOT attention)   */
-#define SAGE2_F_DEBUG_TIMING 64 /* sage2_debug_qk_int32 only: per-phase clock64 stamps (v1/v4/v5/v6) */
-#define SAGE2_F_KERNEL_V1 128 /* use the v1 kernel (b_kv = 128, R written over S; A/B checks)      */
-#define SAGE2_F_DS_SIMT 1024 /* compute Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM */
-#define SAGE2_F_QK_E4M3 2048 /* E4M3-carrier QK^T: INT4 codes stored as E4M3 bytes, S on kind::f8f6f4 */
-                             /* (fp32 accumulator, same integer S); pass to BOTH sage2_prepare and  */
-                             /* sage2_attention.  Invalid with SAGE2_F_INT8 or a KERNEL flag.       */
-#define SAGE2_F_KERNEL_V6 8192 /* use the v6 kernel (one softmax warpgroup per Q tile; A/B)           */
-#define SAGE2_F_KERNEL_V8 4096 /* use the v8 kernel (v6 with each Q tile's softmax split over two   */
-                               /* warpgroups by key columns: 4 softmax warps per SM sub-partition) */
-                               /* No kernel flag: v10 for d = 128, non-causal, N <= 8192, else v8.  */
-#define SAGE2_F_SMOOTH_V 32768 /* optional smooth V (NEXT#2): V' = V - V_m before the     */
-                               /* per-channel FP8 quantization, O + V_m in the epilogue; pass to    */
-                               /* BOTH sage2_prepare and sage2_attention (default kernels only).    */
-#define SAGE2_F_GRAN_BLOCK 262144 /* NEXT#4 ablation: per-block Q/K quantization groups (Q: 128-token */
-                                  /* block, K: 64-token blocks) instead of per-thread  */
-#define SAGE2_F_GRAN_TOKEN 524288 /* NEXT#4 ablation: per-token Q/K quantization groups.  Both flags:  */
-                                  /* d = 128 (v8) only; pass to sage2_prepare AND sage2_attention.    */
-#define SAGE2_F_KERNEL_V5 512 /* use the v5 kernel (b_kv = 64, separate S/R/O, split QK/PV issue)  */
-#define SAGE2_F_KERNEL_V10 16384 /* use the v10 kernel: v8 made persistent (one CTA per SM looping over */
-                                /* (Q-block pair, h_q, b) items); not with QK_E4M3/GRAN/TIMING: EINVAL */
+/* Variant flags (bitwise OR) for sage2_attn_ex / sage2_prepare / sage2_attention.  Flags that change
+ * the preprocessed data (INT8, QK_E4M3, SMOOTH_V, GRAN_*, CAUSAL) must be passed identically to
+ * sage2_prepare and sage2_attention.  Invalid combinations return SAGE2_EINVAL. */
+#define SAGE2_F_CAUSAL 1          /* key <= query mask (C-18); causal workspaces store Delta S triangular */
+#define SAGE2_F_INT8 2            /* SageAttn2-8b: INT8 per-thread Q/K codes (+-127), no Q smoothing     */
+                                  /* (Table 3)                                     */
+#define SAGE2_F_DS_SIMT 1024      /* sage2_prepare: Delta S with the SIMT fp32 kernel instead of the tf32 */
+                                  /* tensor-core GEMM (the default for N <= 2048 anyway)                  */
+#define SAGE2_F_QK_E4M3 2048      /* E4M3-carrier QK^T: the INT4 codes stored as E4M3 bytes and S on      */
+                                  /* kind::f8f6f4 (fp32 accumulator, the same integer S; C-24). */
+                                  /* Not with INT8 or KERNEL_V10.                                         */
+#define SAGE2_F_KERNEL_V8 4096    /* force the v8 attention kernel (csrc/attn8.cuh)                        */
+#define SAGE2_F_KERNEL_V10 16384  /* force the persistent v10 kernel (csrc/attn10.cuh; one CTA per SM      */
+                                  /* looping over (Q-block pair, h_q, b) items).  Not with QK_E4M3/GRAN.  */
+                                  /* No kernel flag: v10 for d = 128, non-causal, N <= 8192 without       */
+                                  /* QK_E4M3 / GRAN flags, else v8 (sage2_attention_kernel answers).      */
+#define SAGE2_F_SMOOTH_V 32768    /* optional smooth V (NEXT#2): V' = V - V_m before the       */
+                                  /* per-channel FP8 quantization, O + V_m in the epilogue                */
+#define SAGE2_F_GRAN_BLOCK 262144 /* NEXT#4 ablation: per-block Q/K quantization groups (Q: 128-token     */
+                                  /* block, K: 64-token blocks) instead of per-thread      */
+#define SAGE2_F_GRAN_TOKEN 524288 /* NEXT#4 ablation: per-token Q/K quantization groups.  GRAN flags:     */
+                                  /* d = 128, kernel v8 only.                                             */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
 const char* sage2_last_cuda_error(void);
@@ -93,8 +86,11 @@ const char* sage2_strerror(int code);
  * N_pad = ceil(N/128)*128).  Returns 0 for invalid shapes. */
 size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int causal);
 
-/* Full forward pass (preprocessing + attention kernel).  Allocates its workspace stream-ordered
- * (cudaMallocAsync / cudaFreeAsync on `stream`).  causal: 0 or 1. */
+/* Full forward pass (preprocessing + attention kernel) -- the north-star entry point.  Allocates its
+ * workspace stream-ordered from the library's per-device pool (cudaMallocFromPoolAsync /
+ * cudaFreeAsync on `stream`); the pool keeps the peak footprint mapped for the next call until
+ * sage2_release_memory().  causal: 0 or 1.  Errors: SAGE2_EINVAL (shape, null / misaligned pointer),
+ * SAGE2_EUNSUPPORTED, SAGE2_ENOMEM, SAGE2_ECUDA. */
 int sage2_attn(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N,
                int d, int causal, void* stream);
 
@@ -119,65 +115,53 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
 /* ---- staged entry points (the same kernels, split so each stage can be timed / inspected) ---- */
 
 /* Workspace layout: writes SAGE2_WS_NREGIONS byte offsets into offsets[] (regions in order:
- * sched(256 B: the v10 kernel's work-item counters, zeroed by sage2_prepare, reset by the kernel),
  * ksum(int64 [B*H_kv*d]), vmax(u32 [B*H_kv*d]), vsum(int64 [B*H_kv*d], smooth V),
  * kbar(f32 [B*H_kv*d]), dv(f32 [B*H_kv*d]), vmean(f32 [B*H_kv*d], smooth V V_m),
- * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][nT][groups]: 32 per-thread groups per block by default; region sized for one per token), qbar(f32 [B*H_q][nT][d]),
- * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][nT][groups]: 8 per 128 keys by default; sized for one per token),
- * vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), qbt(q_bar tf32 big/small split images
- * [B*H_q][ceil(nT/256)][d/32][2][256*128 B], input of the tensor-core Delta S GEMM), ds(f32, scaled
- * by log2(e)/sqrt(d): [B*H_q][nT][N_pad] for non-causal calls; causal calls (SAGE2_F_CAUSAL given to
- * sage2_prepare) store row i of a head with only its 128(i+1) visible keys, at 128*i*(i+1)/2 floats
- * from the head's base 64*nT*(nT+1)*bhq -- half the bytes), end) -- the offsets returned here are
- * the non-causal ones (identical except end).  Tile images are K-major, 128B (d=128) / 64B (d=64)
- * swizzled, the exact shared-memory image the tensor cores read.
- * Returns 0 or SAGE2_EINVAL. */
-#define SAGE2_WS_NREGIONS 16
+ * qhat(int8 tile images [B*H_q][nT][128*d]), dq(f32 [B*H_q][nT][groups]: 32 per-thread groups per
+ * block by default; sized for one per token), qbar(f32 [B*H_q][nT][d]),
+ * khat(int8 tile images [B*H_kv][nT][128*d]), dk(f32 [B*H_kv][nT][groups]: 8 per 128 keys by
+ * default; sized for one per token), vhat(E4M3 V^T tile images [B*H_kv][nT][d*128]), qbt(q_bar tf32
+ * big/small split images [B*H_q][ceil(nT/256)][d/32][2][256*128 B], input of the tensor-core Delta S
+ * GEMM), ds(f32, scaled by log2(e)/sqrt(d): [B*H_q][nT][N_pad] for non-causal calls; causal calls
+ * (SAGE2_F_CAUSAL given to sage2_prepare) store row i of a head with only its 128(i+1) visible keys,
+ * at 128*i*(i+1)/2 floats from the head's base 64*nT*(nT+1)*bhq -- half the bytes), end) -- the
+ * offsets returned here are the non-causal ones (identical except end).  Tile images are K-major,
+ * 128B (d=128) / 64B (d=64) swizzled, the exact shared-memory image the tensor cores read (DESIGN.md
+ * "HBM layout").  Returns 0 or SAGE2_EINVAL. */
+#define SAGE2_WS_NREGIONS 15
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 
 /* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* Attention kernel only (Fig. 3 step 4), on a workspace filled by sage2_prepare with the same
- * shapes and flags.  The workspace is read only, except that the persistent v10 kernel
- * (SAGE2_F_KERNEL_V10) uses the 256-byte sched region as its work counter and leaves it zeroed on
- * exit: v10 calls on one workspace must not run concurrently on different streams. */
-/* Which attention kernel sage2_attention runs for (N, d, flags): 10, 8, 6, 5, 4, 1 or 0 (the
- * version numbers of the SAGE2_F_KERNEL_* selectors; with no selector: 10 for d = 128, non-causal,
- * N <= 8192 without QK_E4M3 / GRAN flags, else 8).  Host-only, no CUDA call; never fails. */
+/* Which attention kernel sage2_attention runs for (N, d, flags): 10 or 8 (SAGE2_F_KERNEL_V10 /
+ * SAGE2_F_KERNEL_V8; with no selector: 10 for d = 128, non-causal, N <= 8192 without QK_E4M3 / GRAN
+ * flags, else 8).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
+/* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263), on a workspace filled by
+ * sage2_prepare with the same shapes and data flags (256-byte aligned, at least
+ * sage2_workspace_bytes).  The workspace is only read: several sage2_attention calls may share one
+ * prepared workspace, also concurrently on different streams.  The persistent v10 kernel takes its
+ * work counters from a per-launch 256-byte block of the library pool. */
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
                     size_t ws_bytes, void* stream);
 
-/* Debug: runs the attention kernel non-causally and additionally writes the raw INT32 QK^T
+/* Debug (parity tests): runs the attention kernel sage2_attention would run for (N, d, flags)
+ * non-causally (a KERNEL flag selects v8 or v10) and additionally writes the raw INT32 QK^T
  * accumulators read back from TMEM to s_int [B*H_q][N_pad][N_pad] (device, caller-owned,
  * 4*B*H_q*N_pad^2 bytes; intended for small N) and, if p_hat is not NULL, the E4M3 codes of
- * P^ = e4m3(448 P~) the kernel fed to the PV MMA, [B*H_q][N_pad][N_pad] bytes (rows of later KV
- * tiles hold the codes computed with the running max at that tile).  out receives the output. */
+ * P^ = e4m3(448 P~) the kernel fed to the PV MMA, [B*H_q][N_pad][N_pad] bytes (the codes of KV tile j
+ * are computed with the running max after tile j).  out receives the output.  GRAN flags: EINVAL. */
 int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H_q, int H_kv, int N, int d,
                          int flags, const void* workspace, size_t ws_bytes, void* stream);
 
-/* Probe (the experiment of P:284-285 repeated on tcgen05).  For each of n
- * fp32 bit patterns D[i] (host array) the accumulator of tcgen05.mma.kind::f8f6f4 (M=128, N=32,
- * K=32, E4M3 x E4M3 -> F32) is initialised to D[i] and one MMA with enable-input-d is issued:
- *   c_zero[i] = bits of (A B + D) with A = B = 0                       (the paper's test)
- *   c_prod[i] = bits of (x[i] * 1.0 + D[i]), x[i] = E4M3 value of prod_vals[i] (one non-zero product)
- * Host arrays, synchronous.  Returns 0 or an error code. */
-int sage2_probe_accumulator(const uint32_t* d_bits, const uint8_t* prod_vals, int n, uint32_t* c_zero,
-                            uint32_t* c_prod);
-
-/* Microbenchmark: issues `iters` back-to-back tcgen05.mma of the given kind (0 = i8 M128 N256 K32,
- * 1 = f8f6f4 E4M3 M128 N256 K32) on every SM and returns the measured dense ops/s in *ops_per_s.
- * Synchronous. */
-int sage2_bench_mma(int kind, int iters, double* ops_per_s);
-
-/* Unit microbenchmarks (per-SM rates per SM clock; synchronous):
- *   0 tcgen05.ld 32x32b bytes/clk, 1 tcgen05.st bytes/clk, 2 MUFU ex2 results/clk,
- *   3 I2F results/clk, 4 FFMA2 lanes/clk, 5 legacy mma.sync m16n8k64 s4 ops/clk (the paper's Ada
- *   INT4 instruction, emulated on sm_100a), 6 legacy mma.sync m16n8k32 s8 ops/clk. */
-int sage2_microbench(int which, int iters, double* per_clk_per_sm);
+/* Returns the device memory the library's stream-ordered pool of the CURRENT device retains
+ * (workspaces of sage2_attn, chunk buffers of sage2_attn_host, per-launch counters; kept mapped
+ * between calls so repeated calls do not re-map gigabytes) to the driver.  Synchronizes the device
+ * first (frees are stream-ordered).  Returns 0 or an error code. */
+int sage2_release_memory(void);
 
 #ifdef __cplusplus
 }

@@ -41,14 +41,14 @@ class OracleConfig:
     b_q: int = 128
     kv_tile: int = 128        # the kernel's b_kv (C-9): 128 (default kernel v6); 64 for v5
     causal: bool = False
-    quant: bool = True
+    quant: bool = True        # False: P~ not quantized (P^ = 448 P~) in attn_block (lossless pin)
     qk_max: int = 7
     smooth_q: bool = True
     smooth_k: bool = True
     pv_mode: int = 0          # 0 fp64 R, 1 fp32 R, 2 FP22-truncated R
     two_level: bool = True
     smooth_v: bool = False
-    p_fp32: bool = True       # P^ decision in the kernel's precision (C-21)
+    p_fp32: bool = False      # True: P^ decision in fp32 (diagnostic of C-21); default fp64 (paper verbatim)
     qk_gran: int = 0          # 0 per-thread (SageAttn2), 1 per-block, 2 per-token (NEXT#4 ablation)
     amb_eta: float = 2.0 ** -12
 

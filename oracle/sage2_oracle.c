@@ -43,7 +43,13 @@ typedef struct {
     int b_q;        /* Q block = smoothing block; 128                        */
     int kv_tile;    /* b_kv, the KV tile of the online softmax; C-9: = kernel's  */
     int causal;     /* key <= query (C-18)                                                      */
-    int quant;      /* 1: SageAttn2 quantized path (Alg. 1); 0: exact mode (P:77 via tiling)   */
+    int quant;      /* orc_attn_block_dbg: 1 = P~ quantized to E4M3 before the PV product
+                       (Alg. 1 line P:256); 0 = quantization of P~ disabled (P^ = 448 P~ exactly),
+                       so on inputs whose Q/K/V codes are lossless (Q' = dQ * codes, ...) the
+                       block loop reduces to exact softmax attention -- the north-star pin
+                       "quantization disabled => exact softmax attention" through the SAME
+                       function that produces every parity reference (tests/test_oracle_lossless.py).
+                       orc_attn_exact_tiled ignores it (it never quantizes).                    */
     int qk_max;     /* 7 = INT4, 127 = INT8 (SageAttn2-8b)                         */
     int smooth_q;   /* subtract per-block mean of Q and add Delta S             */
     int smooth_k;   /* subtract mean of K over all tokens                        */
@@ -51,9 +57,10 @@ typedef struct {
                        every 32-wide K step                            */
     int two_level;  /* 1: R fresh per tile then O = alpha O + R;  0: single level   */
     int smooth_v;   /* optional smooth V; NEXT#2                                    */
-    int p_fp32;     /* 1: the P^ code decision is taken in the kernel's precision (fp32 scores in
-                       base 2, P~*448 rounded to fp32 before the E4M3 cast) -- DESIGN.md C-21;
-                       0: everything in fp64 (the paper's formulas verbatim)                    */
+    int p_fp32;     /* 0 (default): everything in fp64, the paper's formulas verbatim;
+                       1 (diagnostic only): the P^ code decision taken in fp32 in base 2 (scores
+                       rounded to fp32, 2^(s - m + log2 448) rounded to fp32 before the E4M3 cast),
+                       used to measure how many codes an fp32 implementation can flip (C-21)     */
     int qk_gran;    /* Q/K quantization granularity (NEXT#4 ablation):
                        0 per-thread (SageAttn2), 1 per-block (Q: 128-token block, K: 64-token
                        block), 2 per-token (every token its own group)                   */
@@ -416,9 +423,9 @@ int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
                 else if (cfg->p_fp32) p448 = (double)(float)exp2(S[t - j0] - m_new + LOG2_448);
                 else p448 = 448.0 * exp(S[t - j0] - m_new);
                 rowsum += p448 / 448.0;                                          /* C-13 */
-                /* (d) P^ = E4M3(448 * P~) */
+                /* (d) P^ = E4M3(448 * P~); with quant == 0 the cast is skipped (P^ = 448 P~) */
                 uint8_t code = orc_e4m3_encode(p448);
-                double ph = e4m3[code];
+                double ph = cfg->quant ? e4m3[code] : p448;
                 if (phat_out && t < Np) phat_out[(size_t)rr * Np + t] = code;
                 if (p448 > 0.0 && (amb_out || flip_out)) {
                     double ulp;

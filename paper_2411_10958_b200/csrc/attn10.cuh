@@ -2,8 +2,8 @@
 // Same roles, arithmetic and TMEM plan as attn8.cuh (see there), but one CTA per SM loops over work
 // items (Q-block pair, h_q, b) in the v8 order (item w -> pair w % npairs, heaviest causal pairs
 // first within a head, then heads, then batches).  CTA c starts with item c; its producer thread takes
-// every further item from a global counter (p.sched[0], one atomicAdd per item, fetched one item
-// ahead), so faster SMs take more items and causal tails balance like the hardware block scheduler
+// every further item from a global counter (p.sched[0], zeroed by the host right before each launch:
+// a per-launch buffer from the library pool; one atomicAdd per item, fetched one item ahead), so faster SMs take more items and causal tails balance like the hardware block scheduler
 // would; the item index reaches the other roles through a 2-slot shared-memory ring published with
 // the Q barrier's arrive (release) and read after its wait (acquire).  The mbarrier
 // phases (K/V stage ring, per-tile S/P/R handshakes, Q) continue across items, so the next item's Q
@@ -15,8 +15,7 @@
 #include <cuda_fp8.h>
 #include <cstdint>
 
-#include "attn.cuh"
-#include "attn2.cuh"
+#include "common.cuh"
 #include "prep.cuh"
 #include "ptx.cuh"
 
@@ -24,7 +23,7 @@ namespace sage2 {
 
 template <int D>
 struct Attn10Smem {
-    using B2 = Attn2Smem<D>;
+    using B2 = PairSmem<D>;
     static constexpr uint32_t TILE = B2::TILE;
     static constexpr uint32_t Q0 = B2::Q0, Q1 = B2::Q1;
     static constexpr uint32_t ST_K = B2::ST_K, ST_V = B2::ST_V, ST_DS0 = B2::ST_DS0, ST_DS1 = B2::ST_DS1,
@@ -467,14 +466,6 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
     if (warp == 4 * CW) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
-    }
-    if (threadIdx.x == 0) {     // the last CTA out resets the counters for the next launch
-        __threadfence();
-        if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
-            p.sched[0] = 0;
-            p.sched[1] = 0;
-            __threadfence();
-        }
     }
 }
 

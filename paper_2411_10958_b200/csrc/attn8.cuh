@@ -1,12 +1,10 @@
-// attn8.cuh -- SageAttention2 attention kernel v8 for sm_100a.
-// Alg. 1 inner loop, same arithmetic as attn.cuh (v0) / attn6.cuh; b_kv = 128.
+// attn8.cuh -- SageAttention2 attention kernel v8 for sm_100a (Alg. 1 inner loop, PAPER.md:246-263;
+// b_kv = 128).
 //
-// v6 with every Q tile's softmax split over TWO warpgroups by key columns: 16 softmax warps, four
-// per SM sub-partition instead of two.  Measured on v6 (scripts/kernel_timing_v6.py): one softmax
-// warp per tile per sub-partition leaves the MUFU idle ~40% of a tile's exp phase (1740 cycles for
-// 1024 cycles of ex2) and makes the dequant + max phase latency-bound (~900 cycles); with two
-// warps per tile per sub-partition both phases have twice the independent work in flight, and
-// each thread's per-tile work (64 columns) halves.
+// Each Q tile's softmax is split over TWO warpgroups by key columns: 16 softmax warps, four per SM
+// sub-partition.  (Measured against one warpgroup per tile, the former v6: with one softmax warp per
+// tile per sub-partition the MUFU idled ~40% of a tile's exp phase and the dequant + max phase was
+// latency-bound; two warps per tile per sub-partition give both phases twice the independent work.)
 //
 // CTA = two 128-row Q blocks (i0 = 2*pair, i1 = i0 + 1) of one (b, h_q); K^/V^ stages shared.
 // 20 warps (640 threads):
@@ -28,8 +26,7 @@
 #include <cuda_fp8.h>
 #include <cstdint>
 
-#include "attn.cuh"
-#include "attn2.cuh"
+#include "common.cuh"
 #include "prep.cuh"
 #include "ptx.cuh"
 
@@ -37,7 +34,7 @@ namespace sage2 {
 
 template <int D>
 struct Attn8Smem {
-    using B2 = Attn2Smem<D>;
+    using B2 = PairSmem<D>;
     static constexpr uint32_t TILE = B2::TILE;
     static constexpr uint32_t Q0 = B2::Q0, Q1 = B2::Q1;
     static constexpr uint32_t ST_K = B2::ST_K, ST_V = B2::ST_V, ST_DS0 = B2::ST_DS0, ST_DS1 = B2::ST_DS1,

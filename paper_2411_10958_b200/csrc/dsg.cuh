@@ -20,7 +20,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
-#include "attn.cuh"
+#include "common.cuh"
 #include "prep.cuh"
 #include "ptx.cuh"
 

@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, c
         for (int c = 0; c < D; ++c) kp[c] = 0.0f;
     }
     const float* qb = qbar + (size_t)bhq * nT * D;
-    // row offsets as ds_row() (attn.cuh): full rows, or the causal triangular layout (i >= kt only)
+    // row offsets as ds_row() (common.cuh): full rows, or the causal triangular layout (i >= kt only)
     auto row = [&](int i) {
         return tri ? (size_t)bhq * 64 * (size_t)nT * (nT + 1) + 64 * (size_t)i * (i + 1) : ((size_t)bhq * nT + i) * Np;
     };

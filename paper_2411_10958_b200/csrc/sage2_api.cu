@@ -1,32 +1,39 @@
 // sage2_api.cu -- the C ABI of libsage2.so (include/sage2.h): validation, workspace layout,
-// stream-ordered launches of the preprocessing kernels (prep.cuh) and the tcgen05 attention
-// kernel (attn.cuh), plus the accumulator probe and the tensor-core microbenchmark (probe.cuh).
+// stream-ordered launches of the preprocessing kernels (prep.cuh, dsg.cuh) and the tcgen05
+// attention kernels (attn8.cuh, attn10.cuh).
+//
+// Built twice from this one source (paper_2411_10958_b200/build.py):
+//   libsage2.so      the product: only the entry points of include/sage2.h;
+//   libsage2_dev.so  -DSAGE2_DEV: additionally the measurement entry points of include/sage2_dev.h
+//                    (clock64 phase-trace kernel builds, the FP22 accumulator probe, tensor-core and
+//                    unit microbenchmarks).  Never loaded by the product path.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
-#include <vector>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/sage2.h"
-#include "attn.cuh"
-#include "attn2.cuh"
-#include "attn4.cuh"
-#include "attn5.cuh"
-#include "attn6.cuh"
-#include "attn8.cuh"
 #include "attn10.cuh"
-#include "prep.cuh"
+#include "attn8.cuh"
 #include "dsg.cuh"
+#include "prep.cuh"
+#ifdef SAGE2_DEV
+#include "../../include/sage2_dev.h"
 #include "probe.cuh"
+#else
+#define SAGE2_F_DEBUG_TIMING 0   // phase-trace builds exist in libsage2_dev.so only
+#endif
 
 using namespace sage2;
 
 namespace {
 
-constexpr int kVersion = 1;
+constexpr int kVersion = 2;
 thread_local cudaError_t g_last_cuda_error = cudaSuccess;
 
 int cuda_rc() {   // map the launch status to a return code, remembering the CUDA error
@@ -35,27 +42,59 @@ int cuda_rc() {   // map the launch status to a return code, remembering the CUD
     return e == cudaSuccess ? SAGE2_OK : SAGE2_ECUDA;
 }
 
+int current_device(int* dev) {
+    if (cudaGetDevice(dev) != cudaSuccess) return cuda_rc();
+    return (*dev >= 0 && *dev < 64) ? SAGE2_OK : SAGE2_EUNSUPPORTED;
+}
+
+// sm_100 check, cached per device ordinal (a process may drive several GPUs).
 int check_device() {
-    static int state = 0;   // 0 unknown, 1 ok, -1 unsupported
-    static std::mutex mu;
-    std::lock_guard<std::mutex> g(mu);
+    static std::atomic<int> state[64];   // 0 unknown, 1 ok, -1 unsupported
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return cuda_rc();
-    static int cached_dev = -1;
-    if (state == 0 || cached_dev != dev) {
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    int s = state[dev].load(std::memory_order_relaxed);
+    if (s == 0) {
         int major = 0, minor = 0;
         if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
             return cuda_rc();
-        state = (major == 10 && minor == 0) ? 1 : -1;
-        cached_dev = dev;
+        s = (major == 10 && minor == 0) ? 1 : -1;
+        state[dev].store(s, std::memory_order_relaxed);
     }
-    return state == 1 ? SAGE2_OK : SAGE2_EUNSUPPORTED;
+    return s == 1 ? SAGE2_OK : SAGE2_EUNSUPPORTED;
 }
 
+int sm_count(int* nsm) {
+    int dev = 0;
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    if (cudaDeviceGetAttribute(nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return cuda_rc();
+    return SAGE2_OK;
+}
+
+// Opt a kernel into > 48 KB of dynamic shared memory.  cudaFuncSetAttribute is per device (context),
+// so the "done" set is a per-kernel bitmask of device ordinals; concurrent first calls may both set
+// the attribute, which is idempotent.
+template <auto Kernel>
+int configure_smem(uint32_t bytes) {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    const unsigned long long bit = 1ull << dev;
+    if (done.load(std::memory_order_acquire) & bit) return SAGE2_OK;
+    if (cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+        return cuda_rc();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return SAGE2_OK;
+}
+
+// Shapes every kernel supports.  B*H_q and B*H_kv sit on gridDim.y of the preprocessing kernels
+// (limit 65535); N <= 2^22 keeps the exact int64 means (C-1) and the Delta S offsets in range.
 bool shapes_ok(int B, int Hq, int Hkv, int N, int d) {
     return B >= 1 && Hq >= 1 && Hkv >= 1 && N >= 1 && (d == 64 || d == 128) && Hq % Hkv == 0 &&
-           N <= (1 << 22);
+           N <= (1 << 22) && Hq <= 65535 && B <= 65535 && (long long)B * Hq <= 65535;
 }
 
 struct Layout {
@@ -68,7 +107,6 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
     const size_t nT = (size_t)(N + 127) / 128, Np = nT * 128;
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
     const size_t sizes[SAGE2_WS_NREGIONS - 1] = {
-        256,                  // sched (v10 work counters; zeroed by prepare, self-resetting)
         BHk * d * 8,          // ksum
         BHk * d * 4,          // vmax
         BHk * d * 8,          // vsum (smooth V)
@@ -83,7 +121,7 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
         BHk * Np * d,         // vhat
         BHq * ((nT + 255) / 256) * (size_t)(d / 32) * 65536,   // qbt (q_bar tf32 split images)
         // ds last (its size is the only one that depends on causal): full [nT][N_pad] rows, or the
-        // triangular causal layout of ds_row() (attn.cuh), half the bytes
+        // triangular causal layout of ds_row() (common.cuh), half the bytes
         causal ? BHq * 64 * nT * (nT + 1) * 4 : BHq * nT * Np * 4,
     };
     Layout L;
@@ -96,21 +134,26 @@ Layout make_layout(int B, int Hq, int Hkv, int N, int d, bool causal = false) {
     return L;
 }
 
-enum { R_SCHED, R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_QBT, R_DS, R_END };
+enum { R_KSUM, R_VMAX, R_VSUM, R_KBAR, R_DV, R_VMEAN, R_QHAT, R_DQ, R_QBAR, R_KHAT, R_DK, R_VHAT, R_QBT, R_DS, R_END };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool aligned256(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 255) == 0; }
 
-// Library-owned stream-ordered memory pool of the current device for the internal allocations of
-// sage2_attn / sage2_attn_host (workspace, host-path device buffers).  Its release threshold is
-// unlimited, so freed blocks stay mapped for the next call instead of being unmapped and re-mapped
-// (gigabytes per call).  The process's default pool and torch's allocator are not touched.
+// Library-owned stream-ordered memory pool per device for the internal allocations of sage2_attn /
+// sage2_attn_host (workspace, host-path device buffers) and the persistent kernels' per-launch work
+// counters.  Its release threshold is unlimited, so freed blocks stay mapped for the next call instead
+// of being unmapped and re-mapped (gigabytes per call): the pool retains the peak footprint of the
+// calls made so far (about sage2_workspace_bytes of the largest call, plus 3 chunk buffer sets for
+// sage2_attn_host) until sage2_release_memory() trims it.  torch's allocator and the process's default
+// pool are not touched.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+
 cudaMemPool_t lib_pool() {
-    static std::mutex mu;
-    static cudaMemPool_t pools[64] = {};
-    std::lock_guard<std::mutex> g(mu);
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    if (!pools[dev]) {
+    if (current_device(&dev)) return nullptr;
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pools[dev]) {
         cudaMemPoolProps props{};
         props.allocType = cudaMemAllocationTypePinned;
         props.location.type = cudaMemLocationTypeDevice;
@@ -122,9 +165,9 @@ cudaMemPool_t lib_pool() {
         }
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        pools[dev] = pool;
+        g_pools[dev] = pool;
     }
-    return pools[dev];
+    return g_pools[dev];
 }
 
 cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
@@ -132,17 +175,24 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-// The E4M3 carrier only holds the INT4 codes (|c| <= 7) and exists only in the default kernel.
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10;
+constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V |
+                            SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | kKernelFlags
+#ifdef SAGE2_DEV
+                            | SAGE2_F_DEBUG_TIMING
+#endif
+    ;
+
 bool flags_ok(int flags) {
-    const int kernels = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
-                        SAGE2_F_DEBUG_NULLSM | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING;
-    // granularity ablation (NEXT#4): v8 only (no carrier, no kernel selector), not both flags
+    if (flags & ~kKnownFlags) return false;
+    if ((flags & kKernelFlags) == kKernelFlags) return false;
     const int granf = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
     if ((flags & granf) == granf) return false;
-    if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | kernels | SAGE2_F_KERNEL_V6))) return false;
-    // smooth V: the epilogue "+ V_m" exists in the default kernels (v6, v8) only
-    if ((flags & SAGE2_F_SMOOTH_V) && (flags & (kernels & ~SAGE2_F_DEBUG_TIMING))) return false;
-    return !((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | kernels)));
+    // granularity ablation (NEXT#4): v8 at d = 128 only, no carrier
+    if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_KERNEL_V10))) return false;
+    // the E4M3 carrier holds the INT4 codes only (|c| <= 7) and exists in v8 only
+    if ((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | SAGE2_F_KERNEL_V10))) return false;
+    return true;
 }
 
 template <int D>
@@ -153,7 +203,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const int qk_max = (flags & SAGE2_F_INT8) ? 127 : 7;
     const int smooth_q = (flags & SAGE2_F_INT8) ? 0 : 1;   // SageAttn2-8b: no Q smoothing
     const size_t BHk = (size_t)B * Hkv, BHq = (size_t)B * Hq;
-    if (cudaMemsetAsync(ws + L.off[R_SCHED], 0, L.off[R_KBAR] - L.off[R_SCHED], st) != cudaSuccess) return cuda_rc();
+    if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return cuda_rc();
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
     // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
@@ -185,24 +235,16 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
     // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
-    // oracle by the same bound (DESIGN.md §5).
+    // oracle by the same bound (DESIGN.md section 5).
     if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
         k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                     reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
                                                     scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
         return cuda_rc();
     }
-    static bool configured = false;
-    static int nsm = 0;
-    if (!configured) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            cudaFuncSetAttribute(k_delta_s_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, DsgSmem<D>::ALLOC) !=
-                cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
+    int nsm = 0, rc = sm_count(&nsm);
+    if (rc) return rc;
+    if ((rc = configure_smem<k_delta_s_tc<D>>(DsgSmem<D>::ALLOC))) return rc;
     const long long items = (long long)BHq * nT * ((nT + 255) / 256);
     const int grid = (int)std::min<long long>(items, nsm);
     k_delta_s_tc<D><<<grid, 448, DsgSmem<D>::ALLOC, st>>>(
@@ -211,134 +253,90 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP, bool TIMING = false, bool NULLMMA = false>
-int launch_attn2_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn2Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn2<D, CAUSAL, DUMP, TIMING, NULLMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
-    k_attn2<D, CAUSAL, DUMP, TIMING, NULLMMA><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
-    return cuda_rc();
-}
-
-template <int D, bool CAUSAL, bool DUMP, bool NULLSM = false, bool NULLMMA = false, bool TIMING = false>
-int launch_attn4_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn4Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn4<D, CAUSAL, DUMP, NULLSM, NULLMMA, TIMING>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
-    k_attn4<D, CAUSAL, DUMP, NULLSM, NULLMMA, TIMING><<<dim3(p.nT, p.Hq, B), 384, smem, st>>>(p);
-    return cuda_rc();
-}
-
-template <int D, bool CAUSAL, bool DUMP>
-int launch_attn_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = AttnSmem<D>;
-    // D=64 needs less shared memory; request enough to keep one CTA per SM (TMEM: 512 columns).
-    constexpr uint32_t smem = L::ALLOC > 120 * 1024 ? L::ALLOC : 120 * 1024;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn<D, CAUSAL, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
-    k_attn<D, CAUSAL, DUMP><<<dim3(p.nT, p.Hq, B), 192, smem, st>>>(p);
-    return cuda_rc();
-}
-
-int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st);
-
-template <int D, bool CAUSAL, bool DUMP, bool TIMING = false, bool QKF8 = false>
-int launch_attn6_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn2Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn6<D, CAUSAL, DUMP, TIMING, QKF8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
-    k_attn6<D, CAUSAL, DUMP, TIMING, QKF8><<<dim3((p.nT + 1) / 2, p.Hq, B), 384, smem, st>>>(p);
-    return cuda_rc();
-}
-
 template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
 int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn8Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
+    constexpr uint32_t smem = Attn8Smem<D>::ALLOC;
+    int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>>(smem);
+    if (rc) return rc;
     k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
     return cuda_rc();
 }
 
+// The persistent kernel's work counters live in a per-launch buffer from the library pool, zeroed on
+// the launch stream right before the launch: concurrent launches (other streams, shared workspaces)
+// never share counters, and the workspace stays read-only for sage2_attention.
 template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
-int launch_attn10_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn10Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    static int nsm = 0;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn10<D, CAUSAL, DUMP, false, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess)
-            return cuda_rc();
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
-    }
+int launch_attn10_t(AttnParams p, int B, cudaStream_t st) {
+    constexpr uint32_t smem = Attn10Smem<D>::ALLOC;
+    int rc = configure_smem<k_attn10<D, CAUSAL, DUMP, false, TIMING>>(smem);
+    if (rc) return rc;
+    int nsm = 0;
+    if ((rc = sm_count(&nsm))) return rc;
     const long long nitems = (long long)((p.nT + 1) / 2) * p.Hq * B;
     if (nitems > 0x7fffffff) return SAGE2_EINVAL;
     const int grid = (int)(nitems < nsm ? nitems : nsm);   // persistent: one CTA per SM
-    k_attn10<D, CAUSAL, DUMP, false, TIMING><<<grid, 640, smem, st>>>(p, (int)nitems);
-    return cuda_rc();
-}
-
-template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
-int launch_attn5_t(const AttnParams& p, int B, cudaStream_t st) {
-    using L = Attn5Smem<D>;
-    constexpr uint32_t smem = L::ALLOC;
-    static bool configured = false;
-    if (!configured) {
-        if (cudaFuncSetAttribute(k_attn5<D, CAUSAL, DUMP, TIMING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem) != cudaSuccess)
-            return cuda_rc();
-        configured = true;
+    void* ctr = nullptr;
+    if (lib_malloc_async(&ctr, 256, st) != cudaSuccess) {
+        cudaGetLastError();
+        return SAGE2_ENOMEM;
     }
-    k_attn5<D, CAUSAL, DUMP, TIMING><<<dim3((p.nT + 1) / 2, p.Hq, B), 512, smem, st>>>(p);
-    return cuda_rc();
+    if (cudaMemsetAsync(ctr, 0, 8, st) != cudaSuccess) {
+        rc = cuda_rc();
+        cudaFreeAsync(ctr, st);
+        return rc;
+    }
+    p.sched = static_cast<unsigned int*>(ctr);
+    k_attn10<D, CAUSAL, DUMP, false, TIMING><<<grid, 640, smem, st>>>(p, (int)nitems);
+    rc = cuda_rc();
+    if (cudaFreeAsync(ctr, st) != cudaSuccess && rc == SAGE2_OK) rc = cuda_rc();
+    return rc;
 }
 
-
-// the no-kernel-flag dispatch rule shared by launch_attention and sage2_attention_kernel
-bool default_is_v10(int flags, int N, int d) {
-    constexpr int kAny = SAGE2_F_KERNEL_V0 | SAGE2_F_KERNEL_V1 | SAGE2_F_KERNEL_V4 | SAGE2_F_KERNEL_V5 |
-                         SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_DEBUG_NULLSM |
-                         SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_TIMING | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK |
-                         SAGE2_F_GRAN_TOKEN;
-    return !(flags & kAny) && d == 128 && !(flags & SAGE2_F_CAUSAL) && (N + 127) / 128 <= 64;
+// Which kernel a call runs (shared by launch_attention and sage2_attention_kernel).
+int kernel_of(int N, int d, int flags) {
+    if (flags & SAGE2_F_KERNEL_V10) return 10;
+    if (flags & SAGE2_F_KERNEL_V8) return 8;
+    // no selector: the persistent v10 for d = 128, non-causal, N <= 8192 (C2-1K 751 vs 718 TOPS, C2-4K
+    // 1134 vs 1101); v8 elsewhere (from 16K on and for d = 64 / causal v8 is faster)
+    const bool v10 = d == 128 && !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) &&
+                     (N + 127) / 128 <= 64;
+    return v10 ? 10 : 8;
 }
 
-int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags, const uint8_t* ws,
-                     const Layout& L, cudaStream_t st) {
+template <int D>
+int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStream_t st) {
+    const bool causal = (flags & SAGE2_F_CAUSAL) != 0;
+    const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;
+    const int kern = kernel_of(p.N, D, flags);
+#ifdef SAGE2_DEV
+    if (flags & SAGE2_F_DEBUG_TIMING) {   // clock64 phase stamps (non-causal) into s_dump
+        return kern == 10 ? launch_attn10_t<D, false, false, true>(p, B, st)
+                          : launch_attn8_t<D, false, false, false, true>(p, B, st);
+    }
+#endif
+    if (kern == 10) {
+        if (dump) return launch_attn10_t<D, false, true>(p, B, st);
+        return causal ? launch_attn10_t<D, true, false>(p, B, st) : launch_attn10_t<D, false, false>(p, B, st);
+    }
+    if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
+        if constexpr (D != 128) {
+            return SAGE2_EINVAL;
+        } else {
+            if (dump) return SAGE2_EINVAL;
+            if (flags & SAGE2_F_GRAN_TOKEN)
+                return causal ? launch_attn8_t<D, true, false, false, false, 2>(p, B, st)
+                              : launch_attn8_t<D, false, false, false, false, 2>(p, B, st);
+            return causal ? launch_attn8_t<D, true, false, false, false, 1>(p, B, st)
+                          : launch_attn8_t<D, false, false, false, false, 1>(p, B, st);
+        }
+    }
+    if (dump) return f8 ? launch_attn8_t<D, false, true, true>(p, B, st) : launch_attn8_t<D, false, true>(p, B, st);
+    if (f8) return causal ? launch_attn8_t<D, true, false, true>(p, B, st) : launch_attn8_t<D, false, false, true>(p, B, st);
+    return causal ? launch_attn8_t<D, true, false>(p, B, st) : launch_attn8_t<D, false, false>(p, B, st);
+}
+
+int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq, int Hkv, int N, int d, int flags,
+                     const uint8_t* ws, const Layout& L, cudaStream_t st) {
     AttnParams p;
     p.qhat = reinterpret_cast<const int8_t*>(ws + L.off[R_QHAT]);
     p.dq = reinterpret_cast<const float*>(ws + L.off[R_DQ]);
@@ -348,7 +346,7 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.dv = reinterpret_cast<const float*>(ws + L.off[R_DV]);
     p.vmean = (flags & SAGE2_F_SMOOTH_V) ? reinterpret_cast<const float*>(ws + L.off[R_VMEAN]) : nullptr;
     p.ds = reinterpret_cast<const float*>(ws + L.off[R_DS]);
-    p.sched = reinterpret_cast<unsigned int*>(const_cast<uint8_t*>(ws + L.off[R_SCHED]));   // v10 scratch (sage2.h)
+    p.sched = nullptr;
     p.ds_tri = (flags & SAGE2_F_CAUSAL) ? 1 : 0;
     p.out = reinterpret_cast<__half*>(out);
     p.s_dump = s_dump;
@@ -358,136 +356,8 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.N = N;
     p.nT = (N + 127) / 128;
     p.qk_scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
-    const bool causal = (flags & SAGE2_F_CAUSAL) != 0;
-    if (flags & SAGE2_F_KERNEL_V0) {   // the simple one-tile kernel (kept for A/B checks)
-        if (s_dump) {
-            if (d == 64) return launch_attn_t<64, false, true>(p, B, st);
-            return launch_attn_t<128, false, true>(p, B, st);
-        }
-        if (d == 64) return causal ? launch_attn_t<64, true, false>(p, B, st) : launch_attn_t<64, false, false>(p, B, st);
-        return causal ? launch_attn_t<128, true, false>(p, B, st) : launch_attn_t<128, false, false>(p, B, st);
-    }
-    if ((flags & SAGE2_F_DEBUG_TIMING) && (flags & SAGE2_F_KERNEL_V1)) {
-        if (d == 64) return launch_attn2_t<64, false, false, true>(p, B, st);
-        return launch_attn2_t<128, false, false, true>(p, B, st);
-    }
-    if ((flags & SAGE2_F_DEBUG_TIMING) && (flags & SAGE2_F_KERNEL_V5)) {
-        if (d == 64) return launch_attn5_t<64, false, false, true>(p, B, st);
-        return launch_attn5_t<128, false, false, true>(p, B, st);
-    }
-    if ((flags & SAGE2_F_DEBUG_NULLMMA) && !(flags & SAGE2_F_KERNEL_V4)) {
-        if (d == 64) return launch_attn2_t<64, false, false, false, true>(p, B, st);
-        return launch_attn2_t<128, false, false, false, true>(p, B, st);
-    }
-    if (flags & (SAGE2_F_KERNEL_V4 | SAGE2_F_DEBUG_NULLMMA | SAGE2_F_DEBUG_NULLSM))
-        return launch_attention_v4(p, B, d, causal, s_dump != nullptr, flags, st);
-    if (flags & SAGE2_F_KERNEL_V5) {
-        // v5 -- b_kv = 64, separate S / R / O in TMEM, separate QK and PV issuers (attn5.cuh)
-        if (s_dump) {
-            if (d == 64) return launch_attn5_t<64, false, true>(p, B, st);
-            return launch_attn5_t<128, false, true>(p, B, st);
-        }
-        if (d == 64) return causal ? launch_attn5_t<64, true, false>(p, B, st) : launch_attn5_t<64, false, false>(p, B, st);
-        return causal ? launch_attn5_t<128, true, false>(p, B, st) : launch_attn5_t<128, false, false>(p, B, st);
-    }
-    if (flags & SAGE2_F_KERNEL_V10) {   // v10 -- persistent v8 (attn10.cuh)
-        if (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) return SAGE2_EINVAL;
-        if (flags & SAGE2_F_DEBUG_TIMING) {   // softmax phase stamps of CTA 0 (its last item)
-            if (d == 64) return launch_attn10_t<64, false, false, true>(p, B, st);
-            return launch_attn10_t<128, false, false, true>(p, B, st);
-        }
-        if (s_dump) {
-            if (d == 64) return launch_attn10_t<64, false, true>(p, B, st);
-            return launch_attn10_t<128, false, true>(p, B, st);
-        }
-        if (d == 64) return causal ? launch_attn10_t<64, true, false>(p, B, st) : launch_attn10_t<64, false, false>(p, B, st);
-        return causal ? launch_attn10_t<128, true, false>(p, B, st) : launch_attn10_t<128, false, false>(p, B, st);
-    }
-    // default for d = 128, non-causal, N <= 8192: v10 (persistent v8; C2-1K 751 vs 718 TOPS, C2-4K
-    // 1134 vs 1101; from 16K on and for d = 64 / causal v8 is faster: DESIGN.md section 9)
-    if (!s_dump && default_is_v10(flags, N, d)) return launch_attn10_t<128, false, false>(p, B, st);
-    // default otherwise: v8 (C2-32K: d=128 1212 vs 1059 TOPS for v6, causal 1190 vs 1023; d=64 658 vs 644)
-    if ((flags & SAGE2_F_KERNEL_V8) || !(flags & (SAGE2_F_KERNEL_V6 | SAGE2_F_KERNEL_V1))) {
-        // v8 -- v6 with each Q tile's softmax split over two warpgroups by key columns (attn8.cuh)
-        const bool f8 = (flags & SAGE2_F_QK_E4M3) != 0;
-        if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
-            if (d != 128 || s_dump) return SAGE2_EINVAL;
-            if (flags & SAGE2_F_GRAN_TOKEN)
-                return causal ? launch_attn8_t<128, true, false, false, false, 2>(p, B, st)
-                              : launch_attn8_t<128, false, false, false, false, 2>(p, B, st);
-            return causal ? launch_attn8_t<128, true, false, false, false, 1>(p, B, st)
-                          : launch_attn8_t<128, false, false, false, false, 1>(p, B, st);
-        }
-        if (flags & SAGE2_F_DEBUG_TIMING) {
-            if (d == 64) return launch_attn8_t<64, false, false, false, true>(p, B, st);
-            return launch_attn8_t<128, false, false, false, true>(p, B, st);
-        }
-        if (s_dump) {
-            if (d == 64) return f8 ? launch_attn8_t<64, false, true, true>(p, B, st) : launch_attn8_t<64, false, true>(p, B, st);
-            return f8 ? launch_attn8_t<128, false, true, true>(p, B, st) : launch_attn8_t<128, false, true>(p, B, st);
-        }
-        if (d == 64) {
-            if (f8) return causal ? launch_attn8_t<64, true, false, true>(p, B, st) : launch_attn8_t<64, false, false, true>(p, B, st);
-            return causal ? launch_attn8_t<64, true, false>(p, B, st) : launch_attn8_t<64, false, false>(p, B, st);
-        }
-        if (f8) return causal ? launch_attn8_t<128, true, false, true>(p, B, st) : launch_attn8_t<128, false, false, true>(p, B, st);
-        return causal ? launch_attn8_t<128, true, false>(p, B, st) : launch_attn8_t<128, false, false>(p, B, st);
-    }
-    if (flags & SAGE2_F_QK_E4M3) {
-        // v6 with the E4M3-carrier QK^T (codes written as E4M3 by sage2_prepare with the same flag)
-        if (s_dump) {
-            if (d == 64) return launch_attn6_t<64, false, true, false, true>(p, B, st);
-            return launch_attn6_t<128, false, true, false, true>(p, B, st);
-        }
-        if (d == 64)
-            return causal ? launch_attn6_t<64, true, false, false, true>(p, B, st)
-                          : launch_attn6_t<64, false, false, false, true>(p, B, st);
-        return causal ? launch_attn6_t<128, true, false, false, true>(p, B, st)
-                      : launch_attn6_t<128, false, false, false, true>(p, B, st);
-    }
-    if (!(flags & SAGE2_F_KERNEL_V1)) {
-        // v6 (SAGE2_F_KERNEL_V6, and the E4M3-carrier path) -- b_kv = 128, two Q tiles, one softmax
-        // warpgroup per tile, promotion in the softmax warps, MUFU ping-pong
-        if (flags & SAGE2_F_DEBUG_TIMING) {
-            if (d == 64) return launch_attn6_t<64, false, false, true>(p, B, st);
-            return launch_attn6_t<128, false, false, true>(p, B, st);
-        }
-        if (s_dump) {
-            if (d == 64) return launch_attn6_t<64, false, true>(p, B, st);
-            return launch_attn6_t<128, false, true>(p, B, st);
-        }
-        if (d == 64) return causal ? launch_attn6_t<64, true, false>(p, B, st) : launch_attn6_t<64, false, false>(p, B, st);
-        return causal ? launch_attn6_t<128, true, false>(p, B, st) : launch_attn6_t<128, false, false>(p, B, st);
-    }
-    // v1 -- two Q tiles per CTA, b_kv = 128, correction warpgroup, R over S (attn2.cuh)
-    if (s_dump) {
-        if (d == 64) return launch_attn2_t<64, false, true>(p, B, st);
-        return launch_attn2_t<128, false, true>(p, B, st);
-    }
-    if (d == 64) return causal ? launch_attn2_t<64, true, false>(p, B, st) : launch_attn2_t<64, false, false>(p, B, st);
-    return causal ? launch_attn2_t<128, true, false>(p, B, st) : launch_attn2_t<128, false, false>(p, B, st);
-}
-
-// v4: one Q tile per CTA, key columns split over two warpgroups, triple-buffered S/R (attn4.cuh)
-int launch_attention_v4(const AttnParams& p, int B, int d, bool causal, bool dump, int flags, cudaStream_t st) {
-    if (flags & SAGE2_F_DEBUG_TIMING) {   // clock64 stamps of CTA (0,0,0) into s_dump (uint64)
-        if (d == 64) return launch_attn4_t<64, false, false, false, false, true>(p, B, st);
-        return launch_attn4_t<128, false, false, false, false, true>(p, B, st);
-    }
-    if (flags & SAGE2_F_DEBUG_NULLMMA) {  // timing experiment: softmax side only (wrong output)
-        if (d == 64) return launch_attn4_t<64, false, false, false, true>(p, B, st);
-        return launch_attn4_t<128, false, false, false, true>(p, B, st);
-    }
-    if (flags & SAGE2_F_DEBUG_NULLSM) {   // timing experiment: MMA/TMA pipeline only (wrong output)
-        if (d == 64) return launch_attn4_t<64, false, false, true>(p, B, st);
-        return launch_attn4_t<128, false, false, true>(p, B, st);
-    }
-    if (dump) {
-        if (d == 64) return launch_attn4_t<64, false, true>(p, B, st);
-        return launch_attn4_t<128, false, true>(p, B, st);
-    }
-    if (d == 64) return causal ? launch_attn4_t<64, true, false>(p, B, st) : launch_attn4_t<64, false, false>(p, B, st);
-    return causal ? launch_attn4_t<128, true, false>(p, B, st) : launch_attn4_t<128, false, false>(p, B, st);
+    const bool dump = s_dump != nullptr && !(flags & SAGE2_F_DEBUG_TIMING);
+    return d == 64 ? launch_attention_d<64>(p, B, flags, dump, st) : launch_attention_d<128>(p, B, flags, dump, st);
 }
 
 int validate(const void* q, const void* k, const void* v, const void* out, int B, int Hq, int Hkv, int N, int d) {
@@ -508,7 +378,7 @@ const char* sage2_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_
 const char* sage2_strerror(int code) {
     switch (code) {
         case SAGE2_OK: return "ok";
-        case SAGE2_EINVAL: return "invalid argument (shape, pointer, alignment or workspace size)";
+        case SAGE2_EINVAL: return "invalid argument (shape, flags, pointer, alignment or workspace size)";
         case SAGE2_EUNSUPPORTED: return "unsupported device: libsage2 requires sm_100 (B200)";
         case SAGE2_ENOMEM: return "workspace allocation failed";
         case SAGE2_ECUDA: return "CUDA error";
@@ -533,7 +403,7 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q || !k || !v || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
-    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (reinterpret_cast<uintptr_t>(workspace) & 255)) return SAGE2_EINVAL;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned256(workspace)) return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d, (flags & SAGE2_F_CAUSAL) != 0);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -545,22 +415,15 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
                    : launch_prepare<128>(hq, hk, hv, B, H_q, H_kv, N, flags, ws, L, st);
 }
 
-int sage2_attention_kernel(int N, int d, int flags) {
-    if (flags & SAGE2_F_KERNEL_V0) return 0;
-    if (flags & SAGE2_F_KERNEL_V4) return 4;
-    if (flags & SAGE2_F_KERNEL_V5) return 5;
-    if (flags & SAGE2_F_KERNEL_V10) return 10;
-    if (flags & SAGE2_F_KERNEL_V8) return 8;
-    if (flags & SAGE2_F_KERNEL_V6) return 6;
-    if (flags & SAGE2_F_KERNEL_V1) return 1;
-    return default_is_v10(flags, N, d) ? 10 : 8;
-}
+int sage2_attention_kernel(int N, int d, int flags) { return kernel_of(N, d, flags); }
 
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
                     size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
-    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out) || !flags_ok(flags)) return SAGE2_EINVAL;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !workspace || !aligned16(out) || !aligned256(workspace) ||
+        !flags_ok(flags))
+        return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d, (flags & SAGE2_F_CAUSAL) != 0);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     return launch_attention(out, nullptr, nullptr, B, H_q, H_kv, N, d, flags, reinterpret_cast<const uint8_t*>(workspace), L,
@@ -571,7 +434,9 @@ int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H
                          int flags, const void* workspace, size_t ws_bytes, void* stream) {
     int rc = check_device();
     if (rc) return rc;
-    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace || !aligned16(out) || !aligned256(workspace) ||
+        !flags_ok(flags) || (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)))
+        return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
     return launch_attention(out, s_int, p_hat, B, H_q, H_kv, N, d, flags & ~SAGE2_F_CAUSAL,
@@ -617,7 +482,7 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
     // Pipelined over chunks of (b, h_kv) units (one KV head + its H_q/H_kv query heads; contiguous
     // in every [B, H, N, d] tensor and independent): chunk c runs H2D ->
     // prepare -> attention -> D2H on internal stream c % 3, so the copy engines of one chunk overlap
-    // the kernels of the other.  Two device buffer sets (inputs, output, workspace) are reused.
+    // the kernels of the others.  Three device buffer sets (inputs, output, workspace) are reused.
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !q_host || !k_host || !v_host || !out_host) return SAGE2_EINVAL;
@@ -703,6 +568,31 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
     return rc;
 }
 
+int sage2_release_memory(void) {
+    int rc = check_device();
+    if (rc) return rc;
+    int dev = 0;
+    if ((rc = current_device(&dev))) return rc;
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    if (!g_pools[dev]) return SAGE2_OK;
+    if (cudaDeviceSynchronize() != cudaSuccess) return cuda_rc();
+    if (cudaMemPoolTrimTo(g_pools[dev], 0) != cudaSuccess) return cuda_rc();
+    return SAGE2_OK;
+}
+
+#ifdef SAGE2_DEV
+int sage2_dev_trace(void* out, uint64_t* stamps, int B, int H_q, int H_kv, int N, int d, int flags,
+                    const void* workspace, size_t ws_bytes, void* stream) {
+    int rc = check_device();
+    if (rc) return rc;
+    if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !stamps || !workspace || !flags_ok(flags)) return SAGE2_EINVAL;
+    Layout L = make_layout(B, H_q, H_kv, N, d);
+    if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;
+    return launch_attention(out, reinterpret_cast<int32_t*>(stamps), nullptr, B, H_q, H_kv, N, d,
+                            (flags & ~SAGE2_F_CAUSAL) | SAGE2_F_DEBUG_TIMING, reinterpret_cast<const uint8_t*>(workspace),
+                            L, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int sage2_probe_accumulator(const uint32_t* d_bits, const uint8_t* prod_vals, int n, uint32_t* c_zero,
                             uint32_t* c_prod) {
     int rc = check_device();
@@ -724,22 +614,6 @@ int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
     if (which < 0 || which > 9 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
     return run_micro(which, iters, per_clk_per_sm);
 }
-
-int sage2_debug_kernel_attrs(int d, int causal, int* out6) {
-    cudaFuncAttributes a{};
-    const void* f = d == 64 ? (causal ? (const void*)k_attn4<64, true, false> : (const void*)k_attn4<64, false, false>)
-                            : (causal ? (const void*)k_attn4<128, true, false> : (const void*)k_attn4<128, false, false>);
-    out6[0] = (int)cudaFuncGetAttributes(&a, f);
-    out6[1] = a.numRegs;
-    out6[2] = a.maxThreadsPerBlock;
-    out6[3] = (int)a.sharedSizeBytes;
-    out6[4] = a.maxDynamicSharedSizeBytes;
-    int nb = -1;
-    const size_t smem = d == 64 ? Attn4Smem<64>::ALLOC : Attn4Smem<128>::ALLOC;
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 384, smem);
-    out6[5] = nb;
-    return (int)cudaGetLastError();
-}
+#endif
 
 }  // extern "C"

@@ -11,17 +11,45 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SAGE2_LIB overrides the path for A/B experiments (scripts/); the default is the in-tree build.
 LIB_PATH = os.environ.get("SAGE2_LIB") or os.path.join(_HERE, "libsage2.so")
+# measurement-only library (include/sage2_dev.h): phase traces, probes, microbenchmarks
+DEV_LIB_PATH = os.environ.get("SAGE2_DEV_LIB") or os.path.join(_HERE, "libsage2_dev.so")
 
 F_CAUSAL = 1
 F_INT8 = 2
-WS_NREGIONS = 16
-REGIONS = ("sched", "ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "qbt", "ds", "end")
+WS_NREGIONS = 15
+REGIONS = ("ksum", "vmax", "vsum", "kbar", "dv", "vmean", "qhat", "dq", "qbar", "khat", "dk", "vhat", "qbt", "ds", "end")
 
 _lib = None
+_dev = None
 
 
 class Sage2Error(RuntimeError):
     pass
+
+
+def _declare(L):
+    P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    L.sage2_version.restype = I
+    L.sage2_strerror.restype = ctypes.c_char_p
+    L.sage2_strerror.argtypes = [I]
+    L.sage2_last_cuda_error.restype = ctypes.c_char_p
+    L.sage2_workspace_bytes.restype = S
+    L.sage2_workspace_bytes.argtypes = [I] * 6
+    L.sage2_attn.argtypes = [P, P, P, P] + [I] * 6 + [P]
+    L.sage2_attn_ws.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
+    L.sage2_attn_ex.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
+    L.sage2_workspace_layout.argtypes = [I] * 5 + [ctypes.POINTER(S)]
+    L.sage2_prepare.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
+    L.sage2_attention.argtypes = [P] + [I] * 6 + [P, S, P]
+    L.sage2_debug_qk_int32.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
+    L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
+    L.sage2_attention_kernel.argtypes = [I, I, I]
+    L.sage2_attention_kernel.restype = I
+    L.sage2_release_memory.argtypes = []
+    for n in ("sage2_attn", "sage2_attn_ws", "sage2_attn_ex", "sage2_workspace_layout", "sage2_prepare",
+              "sage2_attention", "sage2_debug_qk_int32", "sage2_attn_host", "sage2_release_memory"):
+        getattr(L, n).restype = I
+    return L
 
 
 def lib():
@@ -31,41 +59,34 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise Sage2Error(f"{LIB_PATH} is missing: run `python -m paper_2411_10958_b200.build` "
                              "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
-        P, I, S = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
-        L.sage2_version.restype = I
-        L.sage2_strerror.restype = ctypes.c_char_p
-        L.sage2_strerror.argtypes = [I]
-        L.sage2_last_cuda_error.restype = ctypes.c_char_p
-        L.sage2_workspace_bytes.restype = S
-        L.sage2_workspace_bytes.argtypes = [I] * 6
-        L.sage2_attn.argtypes = [P, P, P, P] + [I] * 6 + [P]
-        L.sage2_attn_ws.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
-        L.sage2_attn_ex.argtypes = [P, P, P, P] + [I] * 6 + [P, S, P]
-        L.sage2_workspace_layout.argtypes = [I] * 5 + [ctypes.POINTER(S)]
-        L.sage2_prepare.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
-        L.sage2_attention.argtypes = [P] + [I] * 6 + [P, S, P]
-        L.sage2_debug_qk_int32.argtypes = [P, P, P] + [I] * 6 + [P, S, P]
-        L.sage2_probe_accumulator.argtypes = [P, P, I, P, P]
-        L.sage2_bench_mma.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
-        L.sage2_attn_host.argtypes = [P, P, P, P] + [I] * 6 + [P]
-        L.sage2_microbench.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
-        L.sage2_microbench.restype = I
-        L.sage2_attention_kernel.argtypes = [I, I, I]
-        L.sage2_attention_kernel.restype = I
-        for n in ("sage2_attn", "sage2_attn_ws", "sage2_attn_ex", "sage2_workspace_layout", "sage2_prepare",
-                  "sage2_attention", "sage2_debug_qk_int32", "sage2_probe_accumulator", "sage2_bench_mma",
-                  "sage2_attn_host"):
-            getattr(L, n).restype = I
-        _lib = L
+        _lib = _declare(ctypes.CDLL(LIB_PATH))
     return _lib
 
 
-def _check(rc):
+def dev_lib():
+    """Load libsage2_dev.so (measurement entry points, include/sage2_dev.h).  Raises if absent."""
+    global _dev
+    if _dev is None:
+        if not os.path.exists(DEV_LIB_PATH):
+            raise Sage2Error(f"{DEV_LIB_PATH} is missing: run `python -m paper_2411_10958_b200.build`")
+        L = _declare(ctypes.CDLL(DEV_LIB_PATH))
+        P, I = ctypes.c_void_p, ctypes.c_int
+        L.sage2_dev_trace.argtypes = [P, P] + [I] * 6 + [P, ctypes.c_size_t, P]
+        L.sage2_probe_accumulator.argtypes = [P, P, I, P, P]
+        L.sage2_bench_mma.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
+        L.sage2_microbench.argtypes = [I, I, ctypes.POINTER(ctypes.c_double)]
+        for n in ("sage2_dev_trace", "sage2_probe_accumulator", "sage2_bench_mma", "sage2_microbench"):
+            getattr(L, n).restype = I
+        _dev = L
+    return _dev
+
+
+def _check(rc, L=None):
     if rc != 0:
-        msg = lib().sage2_strerror(rc).decode()
+        L = L or lib()
+        msg = L.sage2_strerror(rc).decode()
         if rc == -4:
-            msg += ": " + lib().sage2_last_cuda_error().decode()
+            msg += ": " + L.sage2_last_cuda_error().decode()
         raise Sage2Error(f"libsage2 error {rc}: {msg}")
 
 
@@ -151,14 +172,13 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v10": 16384, "v6": 8192, "v8": 4096, "v1": 128, "v5": 512, "v4": 8, "v0": 4}   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096}   # include/sage2.h SAGE2_F_KERNEL_*
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
               smooth_v=False, gran="thread"):
-    """The tcgen05 attention kernel only, on a prepared workspace (kernel: default = v10 (persistent)
-    for d=128 non-causal N <= 8192, v8 otherwise; or an A/B variant;
-    qk_e4m3 must match the prepare() call)."""
+    """The tcgen05 attention kernel only, on a prepared workspace (kernel: "default" = the dispatch
+    rule of sage2_attention_kernel, or "v8" / "v10"; data flags must match the prepare() call)."""
     _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
                                  flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
@@ -170,14 +190,15 @@ def attention_kernel(N, d, causal=False, kernel="default", qk_e4m3=False, gran="
     return int(lib().sage2_attention_kernel(N, d, flags(causal, False, qk_e4m3, False, gran) | KERNEL_FLAGS[kernel]))
 
 
-def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False):
-    """Runs the attention kernel (non-causal) and returns the raw INT32 S = Q^ K^T read from TMEM,
-    [B*Hq, N_pad, N_pad] (and, with_p=True, also the P^ E4M3 codes the kernel produced)."""
+def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False, kernel="default"):
+    """Runs the attention kernel (non-causal; kernel: "default" dispatch rule, "v8" or "v10") and
+    returns the raw INT32 S = Q^ K^T read from TMEM, [B*Hq, N_pad, N_pad] (and, with_p=True, also
+    the P^ E4M3 codes the kernel produced)."""
     Np = (N + 127) // 128 * 128
     s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
     ph = torch.zeros((B * Hq, Np, Np), dtype=torch.uint8, device=out.device) if with_p else None
     _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
-                                      N, d, flags(False, int8, qk_e4m3), workspace.data_ptr(), workspace.numel(),
+                                      N, d, flags(False, int8, qk_e4m3) | KERNEL_FLAGS[kernel], workspace.data_ptr(), workspace.numel(),
                                       _stream()))
     return (s, ph) if with_p else s
 
@@ -202,15 +223,15 @@ def probe_accumulator(d_bits, prod_vals):
     n = d_bits.size
     cz = np.zeros(n, np.uint32)
     cp = np.zeros(n, np.uint32)
-    _check(lib().sage2_probe_accumulator(d_bits.ctypes.data, prod_vals.ctypes.data, n, cz.ctypes.data,
-                                         cp.ctypes.data))
+    _check(dev_lib().sage2_probe_accumulator(d_bits.ctypes.data, prod_vals.ctypes.data, n, cz.ctypes.data,
+                                             cp.ctypes.data), dev_lib())
     return cz, cp
 
 
 def bench_mma(kind, iters=20000):
     """Dense tcgen05 throughput, ops/s.  kind 0 = kind::i8, 1 = kind::f8f6f4 (E4M3)."""
     r = ctypes.c_double()
-    _check(lib().sage2_bench_mma(int(kind), int(iters), ctypes.byref(r)))
+    _check(dev_lib().sage2_bench_mma(int(kind), int(iters), ctypes.byref(r)), dev_lib())
     return r.value
 
 
@@ -222,8 +243,21 @@ MICRO = {0: "tmem_ld_bytes_per_clk_sm", 1: "tmem_st_bytes_per_clk_sm", 2: "mufu_
 
 def microbench(which, iters=4096):
     r = ctypes.c_double()
-    _check(lib().sage2_microbench(int(which), int(iters), ctypes.byref(r)))
+    _check(dev_lib().sage2_microbench(int(which), int(iters), ctypes.byref(r)), dev_lib())
     return r.value
+
+
+def trace(out, workspace, B, Hq, Hkv, N, d, kernel="default"):
+    """clock64 phase stamps of CTA (0,0,0) (dev library): uint64 [16, 64, 16] (role, KV step, slot)."""
+    st = torch.zeros(16 * 64 * 16, dtype=torch.int64, device=out.device)
+    _check(dev_lib().sage2_dev_trace(out.data_ptr(), st.data_ptr(), B, Hq, Hkv, N, d, KERNEL_FLAGS[kernel],
+                                     workspace.data_ptr(), workspace.numel(), _stream()), dev_lib())
+    return st.view(16, 64, 16)
+
+
+def release_memory():
+    """Return the library pool's retained device memory (sage2_release_memory)."""
+    _check(lib().sage2_release_memory())
 
 
 def version():

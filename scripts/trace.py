@@ -1,9 +1,9 @@
-"""Per-phase clock64 stamps of one CTA of the v8 attention kernel (SAGE2_F_DEBUG_TIMING | KERNEL_V8).
+"""Per-phase clock64 stamps of one CTA of the v8 (or v10: KERNEL=v10) attention kernel (dev library:
+sage2.trace).  python scripts/trace.py [N] [d]
 Softmax tile k (thread 0 of its half-0 warpgroup), slots: 0 loop start, 1 S ready, 9 S loaded,
 2 dequant, 3 max exchanged, 4 MUFU turn, 5 P^ written, 6 R ready, 7 R read, 8 promotion done.
 MMA issuer k: 0 kv_full seen, 1 s_free seen, 2 QK committed, 3 P^ seen, 4 PV committed.
 Tile 0, every warp (4 + wq + 4h): slot 7 = its R read (s_free arrival)."""
-import ctypes
 import os
 import sys
 
@@ -16,20 +16,14 @@ from paper_2411_10958_b200 import sage2, synth  # noqa: E402
 B, H = 1, 4
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-flags = 64 + 4096
 q, k, v = synth.make_qkv(B, H, H, N, d, device="cuda")
 ws = sage2.alloc_workspace(B, H, H, N, d)
 sage2.prepare(q, k, v, ws)
 out = torch.empty_like(q)
-buf = torch.zeros(12 * 64 * 16, dtype=torch.int64, device="cuda")
-L = sage2.lib()
-st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 for _ in range(3):
-    rc = L.sage2_debug_qk_int32(out.data_ptr(), buf.data_ptr(), None, B, H, H, N, d, flags, ws.data_ptr(),
-                                ctypes.c_size_t(ws.numel()), st)
-    assert rc == 0, L.sage2_last_cuda_error()
+    buf = sage2.trace(out, ws, B, H, H, N, d, kernel=os.environ.get("KERNEL", "v8"))
 torch.cuda.synchronize()
-t = buf.view(12, 64, 16).cpu().numpy().astype(np.int64)
+t = buf.cpu().numpy().astype(np.int64)
 for j in range(8, 12):
     b = t[0, j, 0]
     print(f"j={j} iter(t0) {t[0, j + 1, 0] - b:5d}")

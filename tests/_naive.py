@@ -81,7 +81,7 @@ def _quant_groups(X, groups, qmax, n_rows):
     return codes, deltas
 
 
-def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=True, gran=0):
+def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=False, gran=0):
     """Q, K, V: [N, d] float16 numpy (one head).  Returns O [N, d] fp64 before fp16 rounding.
 
     p_fp32: scores held as fp32 in base 2 (S log2 e) and 448 P~ rounded to fp32 before the

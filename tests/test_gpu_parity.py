@@ -1,16 +1,18 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
 
-Bar:
+The oracle is the paper-verbatim one (OracleConfig defaults: fp64 scores, P~ = exp(S - m) in fp64
+and P^ = E4M3(448 P~) decided in fp64).  Bar:
   * codes, scales, means (Q^, K^, V^, delta_Q, delta_K, delta_V, q_bar, k_bar): bit-exact;
-  * S_int = Q^ K^T read back from TMEM: bit-exact;
+  * S_int = Q^ K^T read back from TMEM: bit-exact (v8 and v10, up to N = 2048: 16 KV tiles, so
+    the 3-stage K/V ring wraps around several times);
   * Delta S: |gpu - oracle| <= 2e-6 * sum_c |q_bar_c| |K'_tc|   (fp32 FMA chain vs fp64 sum);
-  * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA: identical to the oracle's except where
-    the oracle marks the decision ambiguous (448 P~ within 2^-12 relative of an E4M3 rounding
-    midpoint: the fp32 precision gap between two correct implementations, C-21), and
-    there at most one code apart;
-  * O: elementwise |O_gpu - O_oracle16| <= max(2e-3, 1 fp16 ulp(|O_oracle|)) + F_r, where F_r is
-    the oracle's bound on what flipping row r's ambiguous P^ decisions can move O (0 for almost
-    every row), and CosSim >= 0.9999 (north_star tolerance; O_oracle16 = oracle O rounded to fp16).
+  * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA (diagnostic): identical to the oracle's
+    except where 448 P~ lies within 2^-12 (relative) of an E4M3 rounding midpoint -- there the
+    kernel's fp32 scores / ex2.approx may round the other way (C-21) -- and there at
+    most one code apart;
+  * O: elementwise |O_gpu - O_oracle16| <= max(2e-3, 1 fp16 ulp(|O_oracle|)) and CosSim >= 0.9999
+    (the north-star tolerance; O_oracle16 = oracle O rounded to fp16).  No allowance for the
+    flipped P^ codes: the bar holds with them.
 """
 import math
 
@@ -85,14 +87,18 @@ def test_preprocess_bit_exact(B, Hq, Hkv, N, d, kind, int8):
                     assert np.all(np.abs(got - ds) <= bound + 1e-6 * np.abs(ds))
 
 
-@pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128)])
-def test_s_int_bit_exact(N, d):
+@pytest.mark.parametrize("kernel", ["v8", "v10"])
+@pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128), (1024, 128), (2048, 64), (1900, 128)])
+def test_s_int_bit_exact(N, d, kernel):
+    """Raw S_int read back from TMEM, every Q block against every key: N = 1024 / 2048 / 1900 run
+    8-16 KV tiles through the 3-stage ring (phases wrap), in both the v8 and the persistent v10
+    kernel (v10 carries its ring phases across work items)."""
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=3)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
     sage2.prepare(qg, kg, vg, ws)
     out = torch.empty_like(qg)
-    s = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d)
+    s = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, kernel=kernel)
     torch.cuda.synchronize()
     s = s.cpu().numpy()
     kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
@@ -100,22 +106,25 @@ def test_s_int_bit_exact(N, d):
         for i in range((N + 127) // 128):
             qb = orc.q_block(q.numpy()[0, hq, 128 * i:min(N, 128 * i + 128)])
             ref = orc.s_int_block(qb["qhat"], kv["khat"])
-            assert np.array_equal(s[hq, 128 * i:128 * i + 128].astype(np.int64), ref)
+            assert np.array_equal(s[hq, 128 * i:128 * i + 128].astype(np.int64), ref), (hq, i)
 
 
-@pytest.mark.parametrize("N,d,kind", [(256, 64, "iid"), (384, 128, "structured"), (1000, 128, "structured")])
-def test_phat_codes(N, d, kind):
+@pytest.mark.parametrize("kernel", ["v8", "v10"])
+@pytest.mark.parametrize("N,d,kind", [(256, 64, "iid"), (384, 128, "structured"), (1000, 128, "structured"),
+                                      (2048, 128, "iid"), (1500, 64, "structured")])
+def test_phat_codes(N, d, kind, kernel):
+    """P^ codes the kernel fed to the PV MMA (diagnostic of the C-21 reading)."""
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=7)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
     sage2.prepare(qg, kg, vg, ws)
     out = torch.empty_like(qg)
-    _, ph = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, with_p=True)
+    _, ph = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, with_p=True, kernel=kernel)
     torch.cuda.synchronize()
     ph = ph.cpu().numpy()
     units = [(0, h, i) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(), keep=True, debug=True)
-    n_amb = n_diff = 0
+    n_amb = n_diff = n_tot = 0
     for u, (b, h, i) in enumerate(units):
         dbg = res["inter"][u]["dbg"]
         r1 = min(N, 128 * i + 128) - 128 * i
@@ -127,28 +136,31 @@ def test_phat_codes(N, d, kind):
         assert np.all(np.abs(g[diff].astype(int) - o[diff].astype(int)) <= 1)
         n_amb += int(amb.sum())
         n_diff += int(diff.sum())
-    print(f"P^ codes: {n_diff} differ, all within the {n_amb} ambiguous decisions")
+        n_tot += g.size
+    print(f"P^ codes: {n_diff} of {n_tot} differ, all within the {n_amb} ambiguous decisions")
+    # and the output of the same launch holds the O bar
+    res_o = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units[::3] + [units[-1]], OracleConfig())
+    _compare_out(to_np16(out).astype(np.float64), res_o, units[::3] + [units[-1]], N)
 
 
 def _compare_out(o_gpu, res, units, N):
-    """Returns (max abs err, min cos, rows that needed their flip allowance)."""
-    errs, coss, flipped = [], [], 0
+    """O of the sampled units against the oracle at the north-star bar.  Returns (max abs err,
+    min cos, max err / allowed)."""
+    errs, coss, worst = [], [], 0.0
     for u, (b, h, i) in enumerate(units):
         r0, r1 = 128 * i, min(N, 128 * i + 128)
         ref16 = res["O16"][u, : r1 - r0]
         got = o_gpu[b, h, r0:r1].astype(np.float64)
-        base = np.maximum(2e-3, fp16_ulp(ref16))
-        flip = res["flip"][u, : r1 - r0, None] * (1 + 1e-6) + 1e-7
+        allow = np.maximum(2e-3, fp16_ulp(ref16))
         err = np.abs(got - ref16)
-        ok = err <= base + flip
-        assert np.all(ok), (f"unit {(b, h, i)}: max err {err.max():.3e} at "
-                            f"{np.unravel_index(err.argmax(), err.shape)}, flip bound there "
-                            f"{res['flip'][u, np.unravel_index(err.argmax(), err.shape)[0]]:.3e}")
-        flipped += int(np.any(err > base, axis=1).sum())
+        at = np.unravel_index(err.argmax(), err.shape)
+        assert np.all(err <= allow), (f"unit {(b, h, i)}: max err {err.max():.3e} at {at} "
+                                      f"(oracle {ref16[at]:.6f}, gpu {got[at]:.6f})")
+        worst = max(worst, float((err / allow).max()))
         errs.append(err.max())
         coss.append(orc.cos_sim(res["O"][u, : r1 - r0], got))
     assert min(coss) >= 0.9999, coss
-    return max(errs), min(coss), flipped
+    return max(errs), min(coss), worst
 
 
 OUT_CASES = [
@@ -175,10 +187,9 @@ def test_output_parity(B, Hq, Hkv, N, d, causal, kind):
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     if len(units) > 40:                            # long sequences: every 9th Q block and the last
         units = units[::9] + [units[-1]]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal),
-                                   debug=True)
-    err, cos, flipped = _compare_out(to_np16(out).astype(np.float64), res, units, N)
-    print(f"max|err|={err:.3e} min cos={cos:.8f} rows using flip allowance={flipped}")
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
+    err, cos, worst = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    print(f"max|err|={err:.3e} min cos={cos:.8f} max err/allowed={worst:.3f}")
 
 
 @pytest.mark.parametrize("causal", [False, True])
@@ -189,7 +200,7 @@ def test_int8_variant_parity(causal):
     torch.cuda.synchronize()
     units = [(0, h, i) for h in range(Hq) for i in range(3)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False), debug=True)
+                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False))
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -247,10 +258,10 @@ def test_accuracy_vs_fp32_attention():
         assert cs > min_cos, (kind, cs)
 
 
-@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v10", 128), ("v8", 128), ("v6", 128), ("v1", 128), ("v5", 64), ("v4", 128), ("v0", 128)])
+@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v10", 128), ("v8", 128)])
 @pytest.mark.parametrize("d,causal,N", [(128, False, 384), (64, True, 384), (128, True, 300), (64, False, 200)])
 def test_kernel_variants(kernel, kv_tile, d, causal, N):
-    """Every attention-kernel variant kept for A/B timing matches the oracle run with its b_kv (C-9).
+    """Every attention kernel the library dispatches to matches the oracle run with its b_kv (C-9).
 
     N = 384: three Q tiles, so the two-tile kernels also run a one-tile CTA; N = 300 / 200: ragged
     last tile whose valid rows end inside a warp (the epilogue must stay warp-converged)."""
@@ -263,7 +274,7 @@ def test_kernel_variants(kernel, kv_tile, d, causal, N):
     torch.cuda.synchronize()
     units = [(0, h, i) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, kv_tile=kv_tile), debug=True)
+                                   OracleConfig(causal=causal, kv_tile=kv_tile))
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -281,16 +292,26 @@ def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
     sage2.attention(o8, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v8")
     torch.cuda.synchronize()
     assert torch.equal(o10, o8), "v10 differs from v8"
-    # the work counter resets itself at the end of a launch: a second launch on the same workspace
-    # (no prepare in between) must cover every item again
+    # work counters are per launch (library pool, zeroed before the launch): a second launch on the
+    # same workspace (no prepare in between) covers every item again, and two launches sharing one
+    # prepared workspace on two streams at once do not interfere (the workspace is read-only)
     o10b = torch.full_like(qg, float("nan"))
     sage2.attention(o10b, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
     torch.cuda.synchronize()
-    assert torch.equal(o10b, o8), "second v10 launch differs (work counter not reset)"
-    assert int(ws[sage2.layout(B, Hq, Hkv, N, d)["sched"]:][:8].view(torch.int32).abs().sum()) == 0
+    assert torch.equal(o10b, o8), "second v10 launch differs"
+    o10c, o10d = torch.full_like(qg, float("nan")), torch.full_like(qg, float("nan"))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        sage2.attention(o10c, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+    with torch.cuda.stream(s2):
+        sage2.attention(o10d, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+    torch.cuda.synchronize()
+    assert torch.equal(o10c, o8) and torch.equal(o10d, o8), "concurrent v10 launches interfere"
     nT = (N + 127) // 128
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)][::11]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
     _compare_out(to_np16(o10).astype(np.float64), res, units, N)
 
 
@@ -341,8 +362,7 @@ def test_qk_e4m3_carrier_output_parity(B, Hq, Hkv, N, d, causal, kind):
     torch.cuda.synchronize()
     assert torch.equal(out, ref), "carrier output differs from the kind::i8 output"
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal),
-                                   debug=True)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -381,7 +401,7 @@ def test_smooth_v_output_parity(B, Hq, Hkv, N, d, causal):
     torch.cuda.synchronize()
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, smooth_v=True), debug=True)
+                                   OracleConfig(causal=causal, smooth_v=True))
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -444,7 +464,7 @@ def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
                 assert np.array_equal(g["qhat"][b * Hq + hq, 128 * i:128 * i + 128], qb["qhat"])
                 assert np.array_equal(dq[b * Hq + hq, i].view(np.uint32), qb["dq"].view(np.uint32))
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -467,8 +487,8 @@ def test_random_shapes_fuzz():
         torch.cuda.synchronize()
         units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
         cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8)
-        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
-        err, cos, flipped = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg)
+        err, cos, worst = _compare_out(to_np16(out).astype(np.float64), res, units, N)
         print(f"case {case}: B={B} Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} sv={smooth_v} "
               f"int8={int8}: max|err|={err:.2e} cos={cos:.7f}")
 

@@ -7,8 +7,8 @@ import re
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "sage2.h")).read()
+def declared_symbols(header="sage2.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(sage2_[a-z0-9_]+)\s*\(", src)))
 
@@ -33,6 +33,17 @@ def test_library_builds_loads_and_exports_all_symbols():
     L.sage2_workspace_bytes.restype = ctypes.c_size_t
     assert L.sage2_workspace_bytes(1, 1, 1, 256, 64, 0) > 0
     assert L.sage2_workspace_bytes(1, 1, 1, 256, 96, 0) == 0          # d = 96 invalid
+    assert L.sage2_workspace_bytes(2, 40000, 40000, 256, 64, 0) == 0  # B * H_q > 65535 invalid
+    # the product library carries no measurement entry points
+    for s in declared_symbols("sage2_dev.h"):
+        assert not hasattr(L, s), f"{s} must live in libsage2_dev.so only"
+
+
+def test_dev_library_exports_the_dev_header():
+    from paper_2411_10958_b200 import build
+    L = ctypes.CDLL(build.build(dev=True))
+    for s in declared_symbols() + declared_symbols("sage2_dev.h"):
+        assert hasattr(L, s), s
 
 
 def test_no_cpu_fallback_without_gpu():
@@ -58,4 +69,3 @@ def test_default_kernel_dispatch_rule():
     assert ak(4096, 128, causal=True) == 8 and ak(4096, 64) == 8
     assert ak(4096, 128, qk_e4m3=True) == 8 and ak(4096, 128, gran="block") == 8
     assert ak(32768, 128, kernel="v10") == 10 and ak(1024, 128, kernel="v8") == 8
-    assert ak(1024, 64, kernel="v6") == 6 and ak(1024, 64, kernel="v0") == 0
