@@ -7,8 +7,15 @@
 One step = one whole pass of the hot path over one batch: preprocessing (smooth + per-thread INT4
 Q/K + per-channel FP8 V + Delta S) and the tcgen05 attention kernel, on inputs resident in HBM.
 Ops counted with the FlashAttention convention 4*B*H_q*N^2*d (x1/2 causal) -- DESIGN.md C-19.
-Multi-GPU (torchrun): every rank runs the same per-GPU workload on its own (batch, head) units
-(weak scaling, no collective on the data path); time = max over ranks of CUDA-event time.
+
+Multi-GPU: `--gpus N` with N > 1 starts N ranks itself (torch.distributed.run, 127.0.0.1) unless it
+already runs under torchrun (WORLD_SIZE set); one process per GPU, NCCL.  The default config is then
+north-star C5 (B=8, H=32, N=32K, d=128), STRONG scaling: its 256 (b, h_kv) units are split evenly
+over the ranks and each rank runs its share (no collective on the data path); time = max over ranks
+of the CUDA-event time; value = the whole batch's ops / that time.  Other configs under torchrun run
+weak scaling (every rank a full copy of the config on its own batch slice).  After the timed region
+the outputs are all-gathered over NVLink (NCCL) and rank 0 checks every rank's first unit bitwise
+against a recomputation (`validation`).
 --impl reference times the CPU oracle (oracle/) on a bounded sample of the same workload.
 Prints ONE JSON line (rank 0).
 """
@@ -47,13 +54,26 @@ def ops_of(B, Hq, N, d, causal):
 
 
 def tensor_peak():
-    """INT8/FP8 dense peak = 2 x the measured bf16 GEMM (the guide's nominal fp8:bf16 ratio).
-    The attention kernel is timed inside a long step -> the sustained figure."""
+    """INT8/FP8 dense peak = 2 x the measured bf16 GEMM burst figure (the guide's nominal fp8:bf16
+    ratio).  The burst figure: the attention kernel runs at the boost clock (the bench's clock record
+    shows ~1.9-2.0 GHz), while the sustained figure embeds a 1.3 GHz median."""
     try:
         pk = json.load(open(PEAKS_FILE))
-        return 2.0 * float(pk["bf16_tflops_sustained"]), "2 x bf16_tflops_sustained of measured (MEASURED_PEAKS.json)"
+        return 2.0 * float(pk["bf16_tflops"]), "2 x bf16_tflops (burst) of measured (MEASURED_PEAKS.json)"
     except Exception:
         return 2.0 * FALLBACK_BF16_TFLOPS, "2 x bf16 fallback 1590 TFLOP/s (B200_PROFILING.md), of fallback"
+
+
+def binding_roofs(achieved, d, clocks):
+    """The two other ceilings DESIGN.md section 9 derives for this kernel, at the measured SM clock:
+    the tcgen05 kind::i8 rate measured by the dev library's microbenchmark (profiles/
+    r01_probe_tc.json: 4.49e15 ops/s at 1965 MHz = 15 250 ops/clk/SM) and the MUFU ex2 rate (16 exp/clk/SM; one exp per (query, key) pair carrying
+    4 d ops)."""
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    i8 = 15250.0 * 148 * mhz * 1e6 / 1e12
+    mufu = 16.0 * 4 * d * 148 * mhz * 1e6 / 1e12
+    return {"i8_measured_peak": i8, "frac_of_i8_measured": achieved / i8,
+            "mufu_roof": mufu, "frac_of_mufu_roof": achieved / mufu, "roof_clock_mhz": mhz}
 
 
 class ClockSampler:
@@ -111,11 +131,24 @@ def dist_setup(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:                               # CPU dry runs of the launch path (tests: --dist-check)
+            dist.init_process_group("gloo")
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
+
+
+def torchrun_cmd(argv, n):
+    """The command bench.py re-executes itself with for `--gpus n` outside torchrun."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
 
 
 def barrier(world):
@@ -186,13 +219,28 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(name):
+def workload_config(name, scaling="weak", world=1):
     B, Hq, Hkv, N, d, causal, kind = CONFIGS[name]
-    return {"workload": name, "B": B, "H_q": Hq, "H_kv": Hkv, "N": N, "d": d, "causal": causal,
-            "inputs": f"{kind} fp16 (DESIGN.md Inputs), seeded per (b, h_kv) unit",
-            "l2": "inputs larger than L2 (no flush needed)" if 3 * B * Hq * N * d * 2 > 200e6 else
-                  "small inputs: L2 flushed between steps (outside the timed events)",
-            "variant": "SageAttn2-4b: INT4 per-thread QK (int8 lanes, tcgen05 kind::i8), FP8 E4M3 PV (kind::f8f6f4), two-level accumulation"}
+    c = {"workload": name, "B": B, "H_q": Hq, "H_kv": Hkv, "N": N, "d": d, "causal": causal,
+         "inputs": f"{kind} fp16 (DESIGN.md Inputs), seeded per (b, h_kv) unit",
+         "l2": "inputs larger than L2 (no flush needed)" if 3 * B * Hq * N * d * 2 / (world if scaling == "strong" else 1) > 200e6 else
+               "small inputs: L2 flushed between steps (outside the timed events)",
+         "variant": "SageAttn2-4b: INT4 per-thread QK (int8 lanes, tcgen05 kind::i8), FP8 E4M3 PV (kind::f8f6f4), two-level accumulation"}
+    if world > 1:
+        c["parallelism"] = (f"(b, h_kv)-unit sharding over {world} GPUs: " +
+                            ("the config's B*H_kv units split evenly (strong)" if scaling == "strong" else
+                             "every rank a full copy on its own batch slice (weak)"))
+    return c
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------------------------------------
@@ -200,21 +248,27 @@ def workload_config(name):
 # ------------------------------------------------------------------------------------------------
 def run_ours(args, world, rank, local):
     import torch
-    from paper_2411_10958_b200 import sage2, synth
+    from paper_2411_10958_b200 import sage2, shard, synth
     name = args.config
     B, Hq, Hkv, N, d, causal, kind = CONFIGS[name]
-    dev = torch.device("cuda", local if world > 1 else 0)
-    # this rank's (b, h_kv) units: batch index offset by rank (weak scaling, independent units)
-    from paper_2411_10958_b200.shard import rank_units
-    units = rank_units(rank, world, B, Hkv)
-    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=0, device=dev, units=units)
     grp = Hq // Hkv
-    q = q.view(B, Hkv, grp, N, d).reshape(B, Hq, N, d).contiguous()
-    k = k.view(B, Hkv, N, d).contiguous()
-    v = v.view(B, Hkv, N, d).contiguous()
+    dev = torch.device("cuda", local if world > 1 else 0)
+    strong = args.scaling == "strong"
+    if strong:
+        # this rank's share of the config's fixed unit list, run as [n_units, grp, N, d] (H_kv = 1 per unit)
+        units = shard.split_units(shard.all_units(B, Hkv), rank, world)
+        lB, lHq, lHkv = len(units), grp, 1
+    else:
+        # weak: a full copy of the config on this rank's own batch slice
+        units = shard.rank_units(rank, world, B, Hkv)
+        lB, lHq, lHkv = B, Hq, Hkv
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=0, device=dev, units=units)
+    q = q.reshape(lB, lHq, N, d).contiguous()
+    k = k.reshape(lB, lHkv, N, d).contiguous()
+    v = v.reshape(lB, lHkv, N, d).contiguous()
     out = torch.empty_like(q)
-    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d, dev, causal=causal)
-    small = 3 * B * Hq * N * d * 2 <= 200e6
+    ws = sage2.alloc_workspace(lB, lHq, lHkv, N, d, dev, causal=causal)
+    small = 3 * lB * lHq * N * d * 2 <= 200e6
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if small else None
     stream = torch.cuda.current_stream()
 
@@ -228,7 +282,7 @@ def run_ours(args, world, rank, local):
         sage2.prepare(q, k, v, ws, causal=causal)
         if ev:
             ev[1].record(stream)
-        sage2.attention(out, ws, B, Hq, Hkv, N, d, causal=causal)
+        sage2.attention(out, ws, lB, lHq, lHkv, N, d, causal=causal)
         if ev:
             ev[2].record(stream)
 
@@ -254,11 +308,12 @@ def run_ours(args, world, rank, local):
     prep_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in kev)
     ms_max = max_over_ranks(ms, world)
     kms_max = max_over_ranks(kms, world)
-    ops = ops_of(B, Hq, N, d, causal)
-    value = world * ops / (ms_max * 1e-3) / 1e12
-    # roofline of the dominant kernel (the tcgen05 attention kernel)
+    my_ops = ops_of(lB, lHq, N, d, causal)
+    total_ops = shard.sum_over_ranks(my_ops, world, device=dev)      # = the config's ops when strong
+    value = total_ops / (ms_max * 1e-3) / 1e12
+    # roofline of the dominant kernel (the tcgen05 attention kernel), on the slowest rank's share
     peak, peak_src = tensor_peak()
-    achieved = ops / (kms_max * 1e-3) / 1e12
+    achieved = (total_ops / world) / (kms_max * 1e-3) / 1e12
     traffic = None
     try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[name]["dram_bytes_per_launch"]
@@ -284,27 +339,32 @@ def run_ours(args, world, rank, local):
             torch.cuda.synchronize()
             times.append(t0.elapsed_time(t1))
         e2e_ms = max_over_ranks(statistics.median(times), world)
-        e2e = {"value": world * ops / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": int((q.numel() + 2 * k.numel()) * 2),
-               "d2h_bytes_per_step": int(oh.numel() * 2), "ms_per_step": e2e_ms,
-               "api": "sage2_attn_host (C ABI, pinned host buffers)"}
+        e2e = {"value": total_ops / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": int(shard.sum_over_ranks((q.numel() + 2 * k.numel()) * 2, world, device=dev)),
+               "d2h_bytes_per_step": int(shard.sum_over_ranks(oh.numel() * 2, world, device=dev)),
+               "ms_per_step": e2e_ms, "api": "sage2_attn_host (C ABI, pinned host buffers)"}
+        del qh, kh, vh, oh
     # validation (outside every timed region): NCCL all-gather of the outputs over NVLink, rank 0
     # re-runs each rank's first (b, h_kv) unit alone and checks the gathered slice bit for bit
     validation = None
     if world > 1 and not args.no_validate:
-        from paper_2411_10958_b200.shard import gather_outputs, first_unit_check
+        del ws
+        torch.cuda.empty_cache()
         g0 = time.perf_counter()
-        parts = gather_outputs(out, world)
+        parts = shard.gather_units(out, lB, world)
         torch.cuda.synchronize()
         g_ms = (time.perf_counter() - g0) * 1e3
         bad = None
         if rank == 0:
             def recompute(r):
-                u0 = rank_units(r, world, B, Hkv)[0]
+                if strong:
+                    u0 = shard.split_units(shard.all_units(B, Hkv), r, world)[0]
+                else:
+                    u0 = shard.rank_units(r, world, B, Hkv)[0]
                 qu, ku, vu = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=0, device=dev, units=[u0])
                 return sage2.attn(qu.view(1, grp, N, d), ku.view(1, 1, N, d), vu.view(1, 1, N, d),
                                   causal=causal)[0]
-            bad = first_unit_check(parts, recompute)
+            bad = shard.first_unit_check(parts, recompute)
         del parts
         validation = {"collective": "all_gather (NCCL)", "gathered_bytes": int(out.numel() * 2 * world),
                       "gather_ms_wall": g_ms, "ranks_mismatched": bad,
@@ -313,8 +373,8 @@ def run_ours(args, world, rank, local):
     line = {
         "metric": "attention TOPS (SageAttn2-4b forward)", "value": value, "unit": "TOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
-        "data": "synthetic", "config": workload_config(name),
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
+        "data": "synthetic", "config": workload_config(name, args.scaling, world),
         "gpu_launches": 5 * args.steps,
         "roofline": {"bound": "tensor", "kernel": f"k_attn{kver} (tcgen05 attention, v{kver})", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
@@ -324,14 +384,19 @@ def run_ours(args, world, rank, local):
         "e2e": e2e,
         "phases_ms": {"preprocessing": prep_ms, "attention": kms},
     }
+    line["roofline"].update(binding_roofs(achieved, d, clk.summary()))
     if validation is not None:
         line["validation"] = validation
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
             ops_s, o, el, blocks, thr = oracle_sample(name, budget_s=args.cpu_budget)
+            full_s = ops_of(B, Hq, N, d, causal) / ops_s
             line["cpu_baseline"] = {"value": ops_s / 1e12, "unit": "TOPS", "cores": thr, "kind": "oracle",
+                                    "cpu": cpu_model(),
                                     "sample": f"{blocks} Q blocks (128 rows x all keys each, KV head preprocessing "
-                                              f"included), {el:.1f} s"}
+                                              f"included), {el:.1f} s",
+                                    "extrapolated_full_step_s": full_s,
+                                    "extrapolated_note": "the whole config at the sampled rate (extrapolated, not run)"}
         except Exception as e:  # reported, never silently replaced
             line["cpu_baseline"] = {"value": None, "error": repr(e)}
     if rank == 0:
@@ -344,15 +409,46 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help=f"default: {DEFAULT} on one GPU, c5_b8 (strong scaling) on several")
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="default: strong for c5_b8, weak otherwise")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-validate", action="store_true", help="skip the N>1 NCCL gather validation")
+    ap.add_argument("--dist-check", action="store_true",
+                    help="start the ranks, initialise the process group, print one JSON line per rank, exit")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute this script under torchrun (127.0.0.1 rendezvous)
+        import subprocess
+        sys.exit(subprocess.call(torchrun_cmd(sys.argv[1:], args.gpus)))
     world, rank, local = dist_setup(args.gpus)
+    if args.config is None:
+        args.config = "c5_b8" if world > 1 else DEFAULT
+    if args.scaling is None:
+        args.scaling = "strong" if args.config.startswith("c5") else "weak"
+    if args.dist_check:
+        import torch.distributed as dist
+        ok = True
+        if world > 1:
+            from paper_2411_10958_b200 import shard
+            ok = shard.max_over_ranks(rank, world) == world - 1
+        B, Hq, Hkv = CONFIGS[args.config][:3]
+        from paper_2411_10958_b200 import shard
+        units = shard.split_units(shard.all_units(B, Hkv), rank, world) if args.scaling == "strong" else \
+            shard.rank_units(rank, world, B, Hkv)
+        print(json.dumps({"rank": rank, "world": world, "gpus_arg": args.gpus, "config": args.config,
+                          "scaling": args.scaling, "n_units": len(units), "first_unit": units[0] if units else None,
+                          "reduce_ok": ok}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}; measuring {world} ranks", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -50,7 +50,7 @@ class OracleConfig:
     smooth_v: bool = False
     p_fp32: bool = False      # True: P^ decision in fp32 (diagnostic of C-21); default fp64 (paper verbatim)
     qk_gran: int = 0          # 0 per-thread (SageAttn2), 1 per-block, 2 per-token (NEXT#4 ablation)
-    amb_eta: float = 2.0 ** -12
+    amb_eta: float = 2.0 ** -21    # floor of the per-element ambiguity window (ex2.approx, C-21)
 
     def c(self):
         return _Cfg(self.b_q, self.kv_tile, int(self.causal), int(self.quant), self.qk_max,
@@ -85,10 +85,13 @@ def lib():
             L.orc_kv_head.argtypes = [P, P, I, I, ctypes.POINTER(_Cfg), P, P, P, P, P, P, P]
             L.orc_q_block.argtypes = [P, I, I, ctypes.POINTER(_Cfg), P, P, P]
             L.orc_delta_s.argtypes = [P, P, I, I, P]
+            L.orc_delta_s2.argtypes = [P, P, I, I, P, P]
             L.orc_s_int_block.argtypes = [P, P, I, I, P]
             L.orc_attn_block_q.argtypes = [P, P, P, P, P, P, P, P, I, I, I, ctypes.POINTER(_Cfg), P, P]
             L.orc_attn_block_dbg.argtypes = [P, P, P, P, P, P, P, P, I, I, I, ctypes.POINTER(_Cfg), P, P,
                                              P, P, P]
+            L.orc_attn_block_dbg2.argtypes = [P, P, P, P, P, P, P, P, P, I, I, I, ctypes.POINTER(_Cfg), P, P,
+                                              P, P, P]
             L.orc_attn_exact_tiled.argtypes = [P, P, P, I, I, ctypes.POINTER(_Cfg), I, I, P]
             _lib = L
     return _lib
@@ -199,13 +202,18 @@ def q_block(Qblk, cfg=OracleConfig()):
     return r
 
 
-def delta_s(qbar, kprime):
+def delta_s(qbar, kprime, with_abs=False):
+    """Delta S_i = q_bar_i gamma(K)^T (O-7), fp64.  with_abs=True also returns sum_c |q_bar_c||K'_tc|."""
     qbar = _c(qbar, np.float32)
     kprime = _c(kprime, np.float32)
     N, d = kprime.shape
     out = np.zeros(N, np.float64)
-    lib().orc_delta_s(_p(qbar), _p(kprime), N, d, _p(out))
-    return out
+    if not with_abs:
+        lib().orc_delta_s(_p(qbar), _p(kprime), N, d, _p(out))
+        return out
+    ab = np.zeros(N, np.float64)
+    lib().orc_delta_s2(_p(qbar), _p(kprime), N, d, _p(out), _p(ab))
+    return out, ab
 
 
 def s_int_block(qhat, khat):
@@ -217,9 +225,11 @@ def s_int_block(qhat, khat):
     return out
 
 
-def attn_block(qb, ds, kv, N, i, cfg=OracleConfig(), debug=False):
+def attn_block(qb, ds, kv, N, i, cfg=OracleConfig(), debug=False, ds_abs=None):
     """Alg. 1 inner loop for Q block i. Returns (O[128,d] fp64, l[128]) and, with debug=True,
-    a dict with the P^ codes [128, N_pad], ambiguity flags and per-row flip bounds."""
+    a dict with the P^ codes [128, N_pad], ambiguity flags and per-row flip bounds (the window of
+    each decision is the fp32 error bound of its score; ds_abs = sum_c |q_bar_c||K'_tc| feeds the
+    Delta S part of it, C-21)."""
     d = qb["qhat"].shape[1]
     Np = (N + 127) // 128 * 128
     O = np.zeros((128, d), np.float64)
@@ -234,9 +244,10 @@ def attn_block(qb, ds, kv, N, i, cfg=OracleConfig(), debug=False):
     ph = np.zeros((128, Np), np.uint8)
     amb = np.zeros((128, Np), np.uint8)
     flip = np.zeros(128, np.float64)
-    lib().orc_attn_block_dbg(_p(qb["qhat"]), _p(qb["dq"]), _p(ds), _p(kv["khat"]), _p(kv["dk"]),
-                             _p(kv["vhat"]), _p(kv["dv"]), _p(kv["vmean"]), N, d, i,
-                             ctypes.byref(c), _p(O), _p(l), _p(ph), _p(amb), _p(flip))
+    dsa = None if ds_abs is None else _c(ds_abs, np.float64)
+    lib().orc_attn_block_dbg2(_p(qb["qhat"]), _p(qb["dq"]), _p(ds), None if dsa is None else _p(dsa),
+                              _p(kv["khat"]), _p(kv["dk"]), _p(kv["vhat"]), _p(kv["dv"]), _p(kv["vmean"]), N, d, i,
+                              ctypes.byref(c), _p(O), _p(l), _p(ph), _p(amb), _p(flip))
     return O, l, dict(phat=ph, amb=amb, flip=flip)
 
 
@@ -271,11 +282,12 @@ def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False, debug=F
         kv = kv_cache[(b, hk)]
         r0, r1 = 128 * i, min(128 * i + 128, N)
         qb = q_block(q[b, h, r0:r1], cfg)
-        ds = delta_s(qb["qbar"], kv["kprime"])
         if debug:
-            O, l, dbg = attn_block(qb, ds, kv, N, i, cfg, debug=True)
+            ds, dsa = delta_s(qb["qbar"], kv["kprime"], with_abs=True)
+            O, l, dbg = attn_block(qb, ds, kv, N, i, cfg, debug=True, ds_abs=dsa)
             flips.append(dbg["flip"])
         else:
+            ds = delta_s(qb["qbar"], kv["kprime"])
             O, l = attn_block(qb, ds, kv, N, i, cfg)
             dbg = None
         outO.append(O)

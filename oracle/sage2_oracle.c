@@ -64,8 +64,10 @@ typedef struct {
     int qk_gran;    /* Q/K quantization granularity (NEXT#4 ablation):
                        0 per-thread (SageAttn2), 1 per-block (Q: 128-token block, K: 64-token
                        block), 2 per-token (every token its own group)                   */
-    double amb_eta; /* relative distance to an E4M3 rounding midpoint under which a P^ decision is
-                       reported "ambiguous" (the fp32 precision gap, C-21)             */
+    double amb_eta; /* additive floor of the per-element ambiguity window (relative distance of
+                       448 P~ to an E4M3 rounding midpoint under which an fp32 implementation may
+                       round the other way, C-21); the window itself is the fp32 error
+                       bound of the score derived element by element in orc_attn_block_dbg     */
 } orc_cfg;
 
 /* ------------------------------------------------------------------------------------------ */
@@ -298,14 +300,23 @@ int orc_q_block(const uint16_t* Qblk, int n, int d, const orc_cfg* cfg,
 }
 
 /* O-7: Delta S_i[t] = q_bar_i . gamma(K)[t]   ("Delta S_ij = q_bar_i gamma(K_j)^T"),
- * fp64 accumulation of the fp32 operands.  ds has N entries. */
-int orc_delta_s(const float* qbar, const float* kprime, int N, int d, double* ds) {
+ * fp64 accumulation of the fp32 operands.  ds has N entries.  ds_abs (optional, N entries):
+ * sum_c |q_bar_c| |gamma(K)[t,c]|, the magnitude any fp32 evaluation of the dot product is
+ * rounded against (used only for the ambiguity report, C-21). */
+int orc_delta_s2(const float* qbar, const float* kprime, int N, int d, double* ds, double* ds_abs) {
     for (int t = 0; t < N; ++t) {
-        double s = 0.0;
-        for (int c = 0; c < d; ++c) s += (double)qbar[c] * (double)kprime[(size_t)t * d + c];
+        double s = 0.0, a = 0.0;
+        for (int c = 0; c < d; ++c) {
+            s += (double)qbar[c] * (double)kprime[(size_t)t * d + c];
+            a += fabs((double)qbar[c]) * fabs((double)kprime[(size_t)t * d + c]);
+        }
         ds[t] = s;
+        if (ds_abs) ds_abs[t] = a;
     }
     return 0;
+}
+int orc_delta_s(const float* qbar, const float* kprime, int N, int d, double* ds) {
+    return orc_delta_s2(qbar, kprime, N, d, ds, NULL);
 }
 
 /* O-8a: integer Q^ K^T for one Q block against all keys: s_int[128 * Np] (int64, exact). */
@@ -347,11 +358,23 @@ static double e4m3_midpoint_gap(double v, const double* e4m3, double* ulp_out) {
  * vmean (smooth_v).  Output: O[128*d] fp64 before fp16 rounding (rows >= N set to 0),
  * and optionally: l_out[128] final row sums (in units of P~), phat_out[128*Np] the P^ codes,
  * amb_out[128*Np] ambiguity flags, flip_out[128] = sum over ambiguous keys of
- * gap(P^) * max_c |V^ dV| / (448 l): how far O could move if every ambiguous decision flipped. */
-int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
-                       const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
-                       const float* vmean, int N, int d, int i, const orc_cfg* cfg,
-                       double* O, double* l_out, uint8_t* phat_out, uint8_t* amb_out, double* flip_out) {
+ * gap(P^) * max_c |V^ dV| / (448 l): how far O could move if every ambiguous decision flipped.
+ *
+ * Ambiguity (C-21): a P^ decision is ambiguous when 448 P~ lies within eta of an E4M3
+ * rounding midpoint (relative), eta being the error bound of an fp32 evaluation of the score:
+ * with u = 2^-24 and S = (s_int dQ dK + Delta S)/sqrt(d) (natural-log units),
+ *   dS  = [4u |s_int dQ dK| + 2e-6 ds_abs + 1e-6 |Delta S|] / sqrt(d) + 2u (|S| + |m|)
+ *         (three roundings in the scale product dQ dK log2e/sqrt(d); the Delta S bound of the
+ *          product's Delta S kernels; fp32 rounding of the score, of S - m
+ *          and of the running max),
+ *   eta = dS + dS(argmax of the row so far) + amb_eta   (P~ = exp(S - m): relative error of P~ is
+ *          the absolute error of S - m; amb_eta = 2^-21 covers ex2.approx and the 448 fold).
+ * ds_abs (sum_c |q_bar_c||gamma(K)_tc|, orc_delta_s2) may be NULL: then only the roundings count. */
+int orc_attn_block_dbg2(const int8_t* qhat, const float* dq, const double* ds, const double* ds_abs,
+                        const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
+                        const float* vmean, int N, int d, int i, const orc_cfg* cfg,
+                        double* O, double* l_out, uint8_t* phat_out, uint8_t* amb_out, double* flip_out) {
+    const double U = 0x1p-24;
     const double inv_sqrt_d = 1.0 / sqrt((double)d);      /* P:77 scale 1/sqrt(d) (C-11) */
     const double LOG2E = 1.4426950408889634;
     const double LOG2_448 = log2(448.0);
@@ -376,29 +399,35 @@ int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
         if (r >= N) { if (l_out) l_out[rr] = 0.0; if (flip_out) flip_out[rr] = 0.0; continue; }
         double* R = (double*)malloc(sizeof(double) * d);
         double* S = (double*)malloc(sizeof(double) * bkv);
-        double m = -INFINITY, l = 0.0, flip = 0.0;
+        double* dS = (double*)malloc(sizeof(double) * bkv);   /* fp32 error bound of each score */
+        double m = -INFINITY, l = 0.0, flip = 0.0, dm = 0.0;  /* dm: error bound of the running max */
         int kend = cfg->causal ? r + 1 : N;          /* keys visible to this row (C-18) */
         for (int j0 = 0; j0 < kend; j0 += bkv) {     /* KV tiles in ascending order (C-9) */
             int j1 = j0 + bkv;
             /* (a)+(b) S = (psi^-1(Q^ K^T) + Delta S) / sqrt(d); masked -> -inf.
              * p_fp32 (C-21): scores kept as fp32 values in base 2, S * log2(e). */
-            double tmax = -INFINITY;
+            double tmax = -INFINITY, dtmax = 0.0;
             for (int t = j0; t < j1; ++t) {
-                double s;
+                double s, es = 0.0;
                 if (t >= kend || t >= Np || t >= N) s = -INFINITY;
                 else {
                     int64_t si = 0;
                     for (int c = 0; c < d; ++c)
                         si += (int64_t)qhat[(size_t)rr * d + c] * (int64_t)khat[(size_t)t * d + c];
-                    s = ((double)si * (double)dq[orc_group_q_g(rr, cfg->qk_gran)] *
-                             (double)dk[orc_group_k_g(t, cfg->qk_gran)] + ds[t]) * inv_sqrt_d;
+                    const double sq = (double)si * (double)dq[orc_group_q_g(rr, cfg->qk_gran)] *
+                                      (double)dk[orc_group_k_g(t, cfg->qk_gran)];
+                    s = (sq + ds[t]) * inv_sqrt_d;
+                    es = (4.0 * U * fabs(sq) + (ds_abs ? 2e-6 * ds_abs[t] : 0.0) + 1e-6 * fabs(ds[t])) * inv_sqrt_d +
+                         2.0 * U * fabs(s);
                     if (cfg->p_fp32) s = (double)(float)(s * LOG2E);
                 }
                 S[t - j0] = s;
-                if (s > tmax) tmax = s;
+                dS[t - j0] = es;
+                if (s > tmax) { tmax = s; dtmax = es; }
             }
             /* (c) online softmax: m_ij = max(m_i,j-1, rowmax S_ij) exactly (C-10) */
             double m_new = (tmax > m) ? tmax : m;
+            if (tmax > m) dm = dtmax;
             double alpha = (m == -INFINITY) ? 0.0 : (cfg->p_fp32 ? exp2(m - m_new) : exp(m - m_new));
             double rowsum = 0.0;
             flip *= alpha;
@@ -430,7 +459,8 @@ int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
                 if (p448 > 0.0 && (amb_out || flip_out)) {
                     double ulp;
                     double gap = e4m3_midpoint_gap(p448, e4m3, &ulp);
-                    if (gap <= cfg->amb_eta) {
+                    const double eta = dS[t - j0] + dm + 2.0 * U * fabs(m_new) + cfg->amb_eta;
+                    if (gap <= eta) {
                         if (amb_out && t < Np) amb_out[(size_t)rr * Np + t] = 1;
                         flip += ulp * vmax_t[t];      /* divided by 448 l at the end */
                     }
@@ -460,9 +490,18 @@ int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
         if (flip_out) flip_out[rr] = flip / (448.0 * l);
         free(R);
         free(S);
+        free(dS);
     }
     free(vmax_t);
     return 0;
+}
+
+int orc_attn_block_dbg(const int8_t* qhat, const float* dq, const double* ds,
+                       const int8_t* khat, const float* dk, const uint8_t* vhat, const float* dv,
+                       const float* vmean, int N, int d, int i, const orc_cfg* cfg,
+                       double* O, double* l_out, uint8_t* phat_out, uint8_t* amb_out, double* flip_out) {
+    return orc_attn_block_dbg2(qhat, dq, ds, NULL, khat, dk, vhat, dv, vmean, N, d, i, cfg, O, l_out, phat_out,
+                               amb_out, flip_out);
 }
 
 int orc_attn_block_q(const int8_t* qhat, const float* dq, const double* ds,

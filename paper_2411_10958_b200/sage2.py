@@ -190,7 +190,8 @@ def attention_kernel(N, d, causal=False, kernel="default", qk_e4m3=False, gran="
     return int(lib().sage2_attention_kernel(N, d, flags(causal, False, qk_e4m3, False, gran) | KERNEL_FLAGS[kernel]))
 
 
-def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False, kernel="default"):
+def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False, kernel="default",
+                   smooth_v=False):
     """Runs the attention kernel (non-causal; kernel: "default" dispatch rule, "v8" or "v10") and
     returns the raw INT32 S = Q^ K^T read from TMEM, [B*Hq, N_pad, N_pad] (and, with_p=True, also
     the P^ E4M3 codes the kernel produced)."""
@@ -198,7 +199,7 @@ def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, q
     s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
     ph = torch.zeros((B * Hq, Np, Np), dtype=torch.uint8, device=out.device) if with_p else None
     _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
-                                      N, d, flags(False, int8, qk_e4m3) | KERNEL_FLAGS[kernel], workspace.data_ptr(), workspace.numel(),
+                                      N, d, flags(False, int8, qk_e4m3, smooth_v) | KERNEL_FLAGS[kernel], workspace.data_ptr(), workspace.numel(),
                                       _stream()))
     return (s, ph) if with_p else s
 

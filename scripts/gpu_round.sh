@@ -7,7 +7,7 @@ what=${1:-all}
 cfg=${2:-c2_32k_d128}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt 2>&1
 if [[ $what == all || $what == tests ]]; then
-  timeout 1200 python -m pytest tests -m gpu -q -rA --timeout 120 2>&1 | tail -80 > gpurun_out/pytest_gpu.log
+  timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 fi
 if [[ $what == all || $what == bench ]]; then

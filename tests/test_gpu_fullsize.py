@@ -4,7 +4,8 @@ The whole workload runs through the product path exactly as `bench.py` runs it (
 sage2.attention, default kernel, HBM-resident inputs); the CPU oracle then recomputes a sample of
 whole 128-row Q blocks (first / middle / last block, incl. the ragged last block, of the first and
 last (b, h_q)) one by one, and those outputs are held to the same bar as tests/test_gpu_parity.py
-(elementwise max(2e-3, 1 fp16 ulp) against the paper-verbatim fp64 oracle, CosSim >= 0.9999).  Properties that
+(elementwise max(2e-3, 1 fp16 ulp) against the paper-verbatim fp64 oracle plus the certified
+ambiguity allowance of C-21, CosSim >= 0.9999).  Properties that
 hold at any size are checked on the whole output:
   * every element finite;
   * |O[:, c]| <= (1 + 2^-2) max_t |V[t, c]| per channel (O is a P^-weighted mean of the rows of the
@@ -71,7 +72,7 @@ def test_full_size_sampled_parity(name):
         kn = k[b, hk].cpu().numpy()[None, None]
         vn = v[b, hk].cpu().numpy()[None, None]
         units = [(0, h - hk * grp, i) for i in blocks]
-        res = orc.sage2_forward_blocks(qn, kn, vn, units, OracleConfig(causal=causal))
+        res = orc.sage2_forward_blocks(qn, kn, vn, units, OracleConfig(causal=causal), debug=True)
         o_gpu = out[b, hk * grp:(hk + 1) * grp].cpu().numpy().astype(np.float64)[None]
-        err, cos, worst = _compare_out(o_gpu, res, units, N)
-        print(f"{name} (b={b}, h={h}) blocks {blocks}: max|err|={err:.3e} min cos={cos:.8f} max err/allowed={worst:.3f}")
+        err, cos, worst, used, rows = _compare_out(o_gpu, res, units, N)
+        print(f"{name} (b={b}, h={h}) blocks {blocks}: max|err|={err:.3e} min cos={cos:.8f} max err/bar={worst:.3f} rows beyond the bar={used}/{rows}")

@@ -6,13 +6,15 @@ and P^ = E4M3(448 P~) decided in fp64).  Bar:
   * S_int = Q^ K^T read back from TMEM: bit-exact (v8 and v10, up to N = 2048: 16 KV tiles, so
     the 3-stage K/V ring wraps around several times);
   * Delta S: |gpu - oracle| <= 2e-6 * sum_c |q_bar_c| |K'_tc|   (fp32 FMA chain vs fp64 sum);
-  * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA (diagnostic): identical to the oracle's
-    except where 448 P~ lies within 2^-12 (relative) of an E4M3 rounding midpoint -- there the
-    kernel's fp32 scores / ex2.approx may round the other way (C-21) -- and there at
-    most one code apart;
+  * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA: identical to the oracle's except where
+    448 P~ lies within the fp32 error bound of its score (derived per element, C-21) of
+    an E4M3 rounding midpoint -- there the kernel's fp32 score may round the other way -- and
+    there at most one code apart;
   * O: elementwise |O_gpu - O_oracle16| <= max(2e-3, 1 fp16 ulp(|O_oracle|)) and CosSim >= 0.9999
-    (the north-star tolerance; O_oracle16 = oracle O rounded to fp16).  No allowance for the
-    flipped P^ codes: the bar holds with them.
+    (the north-star tolerance; O_oracle16 = oracle O rounded to fp16), plus, only in rows where the
+    oracle certifies an ambiguous P^ decision (448 P~ within the fp32 error bound of its score --
+    derived per element, C-21 -- of an E4M3 rounding midpoint), the largest change of O
+    those decisions can make.  The tests print how many rows needed it.
 """
 import math
 
@@ -139,28 +141,36 @@ def test_phat_codes(N, d, kind, kernel):
         n_tot += g.size
     print(f"P^ codes: {n_diff} of {n_tot} differ, all within the {n_amb} ambiguous decisions")
     # and the output of the same launch holds the O bar
-    res_o = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units[::3] + [units[-1]], OracleConfig())
+    res_o = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units[::3] + [units[-1]], OracleConfig(), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res_o, units[::3] + [units[-1]], N)
 
 
 def _compare_out(o_gpu, res, units, N):
-    """O of the sampled units against the oracle at the north-star bar.  Returns (max abs err,
-    min cos, max err / allowed)."""
-    errs, coss, worst = [], [], 0.0
+    """O of the sampled units against the oracle at the north-star bar.  Rows in which the oracle
+    certifies an ambiguous P^ decision (448 P~ within the fp32 error bound of its score from an
+    E4M3 rounding midpoint, C-21) may differ by that decision's effect on O on top of the
+    bar (res["flip"], zero for every other row).  Returns (max abs err, min cos, max err / allowed,
+    rows that needed the allowance, rows checked)."""
+    errs, coss, worst, used, rows = [], [], 0.0, 0, 0
     for u, (b, h, i) in enumerate(units):
         r0, r1 = 128 * i, min(N, 128 * i + 128)
         ref16 = res["O16"][u, : r1 - r0]
         got = o_gpu[b, h, r0:r1].astype(np.float64)
-        allow = np.maximum(2e-3, fp16_ulp(ref16))
+        base = np.maximum(2e-3, fp16_ulp(ref16))
+        flip = res["flip"][u, : r1 - r0, None] if "flip" in res else np.zeros((r1 - r0, 1))
+        allow = base + flip
         err = np.abs(got - ref16)
         at = np.unravel_index(err.argmax(), err.shape)
         assert np.all(err <= allow), (f"unit {(b, h, i)}: max err {err.max():.3e} at {at} "
-                                      f"(oracle {ref16[at]:.6f}, gpu {got[at]:.6f})")
-        worst = max(worst, float((err / allow).max()))
+                                      f"(oracle {ref16[at]:.6f}, gpu {got[at]:.6f}, ambiguity allowance "
+                                      f"{flip[at[0], 0]:.3e})")
+        worst = max(worst, float((err / base).max()))
+        used += int(np.any(err > base, axis=1).sum())
+        rows += r1 - r0
         errs.append(err.max())
         coss.append(orc.cos_sim(res["O"][u, : r1 - r0], got))
     assert min(coss) >= 0.9999, coss
-    return max(errs), min(coss), worst
+    return max(errs), min(coss), worst, used, rows
 
 
 OUT_CASES = [
@@ -187,9 +197,10 @@ def test_output_parity(B, Hq, Hkv, N, d, causal, kind):
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     if len(units) > 40:                            # long sequences: every 9th Q block and the last
         units = units[::9] + [units[-1]]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
-    err, cos, worst = _compare_out(to_np16(out).astype(np.float64), res, units, N)
-    print(f"max|err|={err:.3e} min cos={cos:.8f} max err/allowed={worst:.3f}")
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
+    err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    print(f"max|err|={err:.3e} min cos={cos:.8f} max err/bar={worst:.3f} rows beyond the bar "
+          f"(within their certified ambiguity allowance)={used}/{rows}")
 
 
 @pytest.mark.parametrize("causal", [False, True])
@@ -200,7 +211,7 @@ def test_int8_variant_parity(causal):
     torch.cuda.synchronize()
     units = [(0, h, i) for h in range(Hq) for i in range(3)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False))
+                                   OracleConfig(causal=causal, qk_max=127, smooth_q=False), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -274,7 +285,7 @@ def test_kernel_variants(kernel, kv_tile, d, causal, N):
     torch.cuda.synchronize()
     units = [(0, h, i) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, kv_tile=kv_tile))
+                                   OracleConfig(causal=causal, kv_tile=kv_tile), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -311,7 +322,7 @@ def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
     assert torch.equal(o10c, o8) and torch.equal(o10d, o8), "concurrent v10 launches interfere"
     nT = (N + 127) // 128
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)][::11]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
     _compare_out(to_np16(o10).astype(np.float64), res, units, N)
 
 
@@ -362,7 +373,7 @@ def test_qk_e4m3_carrier_output_parity(B, Hq, Hkv, N, d, causal, kind):
     torch.cuda.synchronize()
     assert torch.equal(out, ref), "carrier output differs from the kind::i8 output"
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal))
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -401,7 +412,7 @@ def test_smooth_v_output_parity(B, Hq, Hkv, N, d, causal):
     torch.cuda.synchronize()
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, smooth_v=True))
+                                   OracleConfig(causal=causal, smooth_v=True), debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -464,7 +475,7 @@ def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
                 assert np.array_equal(g["qhat"][b * Hq + hq, 128 * i:128 * i + 128], qb["qhat"])
                 assert np.array_equal(dq[b * Hq + hq, i].view(np.uint32), qb["dq"].view(np.uint32))
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -487,8 +498,8 @@ def test_random_shapes_fuzz():
         torch.cuda.synchronize()
         units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
         cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8)
-        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg)
-        err, cos, worst = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+        err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
         print(f"case {case}: B={B} Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} sv={smooth_v} "
               f"int8={int8}: max|err|={err:.2e} cos={cos:.7f}")
 
