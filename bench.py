@@ -178,7 +178,9 @@ def oracle_sample(cfg_name, budget_s, max_blocks=None):
     q, k, v = q.numpy(), k.numpy()[:, None], v.numpy()[:, None]
     nT = (N + 127) // 128
     order = [nT - 1, nT // 2, 0] + [t for t in range(nT - 2, 0, -1) if t != nT // 2]
-    cfg = OracleConfig(causal=causal)
+    from paper_2411_10958_b200 import sage2
+    # the oracle's KV tile is the kernel's b_kv (reading C-9): 64 for the d = 64 kernel v12
+    cfg = OracleConfig(causal=causal, kv_tile=64 if sage2.attention_kernel(N, d, causal=causal) == 12 else 128)
     done_ops, t0, blocks = 0.0, time.perf_counter(), 0
     for i in order:
         r0, r1 = 128 * i, min(N, 128 * i + 128)

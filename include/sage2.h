@@ -63,8 +63,10 @@ extern "C" {
 #define SAGE2_F_KERNEL_V8 4096    /* force the v8 attention kernel (csrc/attn8.cuh)                        */
 #define SAGE2_F_KERNEL_V10 16384  /* force the persistent v10 kernel (csrc/attn10.cuh; one CTA per SM      */
                                   /* looping over (Q-block pair, h_q, b) items).  Not with QK_E4M3/GRAN.  */
-                                  /* No kernel flag: v10 for d = 128, non-causal, N <= 8192 without       */
-                                  /* QK_E4M3 / GRAN flags, else v8 (sage2_attention_kernel answers).      */
+                                  /* No kernel flag: sage2_attention_kernel answers which kernel runs.    */
+#define SAGE2_F_KERNEL_V12 131072 /* force the v12 kernel (csrc/attn12.cuh, d = 64 only: four Q tiles per  */
+                                  /* CTA, b_kv = 64 -- the oracle's kv_tile is then 64, reading C-9).      */
+                                  /* Not with QK_E4M3 / GRAN flags.                                       */
 #define SAGE2_F_SMOOTH_V 32768    /* optional smooth V (NEXT#2): V' = V - V_m before the       */
                                   /* per-channel FP8 quantization, O + V_m in the epilogue                */
 #define SAGE2_F_GRAN_BLOCK 262144 /* NEXT#4 ablation: per-block Q/K quantization groups (Q: 128-token     */
@@ -135,9 +137,9 @@ int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offse
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* Which attention kernel sage2_attention runs for (N, d, flags): 10 or 8 (SAGE2_F_KERNEL_V10 /
- * SAGE2_F_KERNEL_V8; with no selector: 10 for d = 128, non-causal, N <= 8192 without QK_E4M3 / GRAN
- * flags, else 8).  Host-only, no CUDA call; never fails. */
+/* Which attention kernel sage2_attention runs for (N, d, flags): 12, 10 or 8 (SAGE2_F_KERNEL_V12 /
+ * _V10 / _V8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64 non-causal, 10 for d = 128
+ * non-causal N <= 8192; 8 otherwise).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
 /* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263), on a workspace filled by

@@ -18,7 +18,7 @@ extern "C" {
 
 /* clock64 phase trace of the attention kernel sage2_attention would run (non-causal; a KERNEL flag
  * selects v8 / v10): stamps of CTA (0,0,0) written to `stamps` (device, caller-owned, zeroed,
- * uint64 [16 roles][64 KV steps][16 slots]; the slot meaning is in the kernel source (ts / tss
+ * uint64 [32 roles][64 KV steps][16 slots]; the slot meaning is in the kernel source (ts / tss
  * calls)).  out receives the output. */
 int sage2_dev_trace(void* out, uint64_t* stamps, int B, int H_q, int H_kv, int N, int d, int flags,
                     const void* workspace, size_t ws_bytes, void* stream);
@@ -40,7 +40,8 @@ int sage2_bench_mma(int kind, int iters, double* ops_per_s);
  *   0 tcgen05.ld 32x32b bytes/clk, 1 tcgen05.st bytes/clk, 2 MUFU ex2 results/clk,
  *   3 I2F results/clk, 4 FFMA2 lanes/clk, 5 legacy mma.sync m16n8k64 s4 ops/clk (the paper's Ada
  *   INT4 instruction, emulated on sm_100a), 6 legacy mma.sync m16n8k32 s8 ops/clk,
- *   7 F2FP e4m3x2 elements/clk, 8 FMNMX3 /clk, 9 the softmax instruction mix elements/clk. */
+ *   7 F2FP e4m3x2 elements/clk, 8 FMNMX3 /clk, 9 the softmax instruction mix elements/clk,
+ *   10 tcgen05.ld 16x64b bytes/clk, 11 tcgen05.st 16x64b bytes/clk. */
 int sage2_microbench(int which, int iters, double* per_clk_per_sm);
 
 #ifdef __cplusplus

@@ -32,6 +32,10 @@
 
 namespace sage2 {
 
+#ifndef SAGE2_PSPLIT
+#define SAGE2_PSPLIT 1   // hand P^ to the PV MMA in two halves (A/B builds: 0 = one hand-off per tile)
+#endif
+
 template <int D>
 struct Attn8Smem {
     using B2 = PairSmem<D>;
@@ -43,7 +47,7 @@ struct Attn8Smem {
     static constexpr uint32_t XM = P1 + 16384;              // float xm[2 tiles][2 buf][2 halves][128]
     static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;  // float xl[2 tiles][2 halves][128]
     static constexpr uint32_t BAR = XL + 2 * 2 * 128 * 4;
-    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 8;
+    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 10;
     static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
     static constexpr uint32_t BYTES = TMEMPTR + 16;
     static constexpr uint32_t ALLOC = BYTES + 1024;
@@ -93,6 +97,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     auto bar_p_full = [&](int k) { return bar0 + 8 * (3 + 2 * kStages2 + k); };
     auto bar_r_full = [&](int k) { return bar0 + 8 * (5 + 2 * kStages2 + k); };
     auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * kStages2 + k); };
+    auto bar_pa_full = [&](int k) { return bar0 + 8 * (9 + 2 * kStages2 + k); };   // first halves of P^
     auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
 
     if (threadIdx.x == 0) {
@@ -104,6 +109,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
         for (int k = 0; k < 2; ++k) {
             mbar_init(bar_s_full(k), 1);
             mbar_init(bar_p_full(k), 256);
+            mbar_init(bar_pa_full(k), 256);
             mbar_init(bar_r_full(k), 1);
             mbar_init(bar_s_free(k), 256);
         }
@@ -172,12 +178,26 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 }
                 mma_commit_w(bar_s_full(k));
                 if (lane == 0) ts(2 + k, j, 2);
-                mbar_wait(bar_p_full(k), j & 1);                    // softmax_k(j) wrote P^_k
-                if (lane == 0) ts(2 + k, j, 3);
-                tc_fence_after();
                 const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
+                if (SAGE2_PSPLIT) {
+                    // each key half's first 32 codes (P^ columns 0-31 and 64-95: K steps 0 and 2) are
+                    // multiplied while the softmax still exponentiates the second 32
+                    mbar_wait(bar_pa_full(k), j & 1);
+                    if (lane == 0) ts(2 + k, j, 3);
+                    tc_fence_after();
+                    mma_f8f6f4_w(tS, pdesc + 0, vdesc + 0, IDPV, 0);
+                    mma_f8f6f4_w(tS, pdesc + 4, vdesc + 4, IDPV, 1);
+                    mbar_wait(bar_p_full(k), j & 1);                // softmax_k(j) wrote all of P^_k
+                    tc_fence_after();
+                    mma_f8f6f4_w(tS, pdesc + 2, vdesc + 2, IDPV, 1);
+                    mma_f8f6f4_w(tS, pdesc + 6, vdesc + 6, IDPV, 1);
+                } else {
+                    mbar_wait(bar_p_full(k), j & 1);                // softmax_k(j) wrote P^_k
+                    if (lane == 0) ts(2 + k, j, 3);
+                    tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                    for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                }
                 mma_commit_w(bar_r_full(k));
                 mma_commit_w(bar_kv_empty(s));
                 if (lane == 0) ts(2 + k, j, 4);
@@ -312,6 +332,11 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                     if (DUMP && p.p_dump)
                         *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h + c0) =
                             make_uint4(w[0], w[1], w[2], w[3]);
+                    if (SAGE2_PSPLIT && c0 == 16) {                  // this half's first 32 codes are in smem
+                        fence_proxy_async_smem();
+                        tc_fence_before();
+                        mbar_arrive(bar_pa_full(k));
+                    }
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();

@@ -178,7 +178,8 @@ template <int WHICH>
 __global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long* cyc, float* sink) {
     __shared__ uint32_t tptr;
     const int warp = threadIdx.x / 32;
-    if (WHICH <= 1) {
+    constexpr bool TM = WHICH <= 1 || WHICH == 10 || WHICH == 11;
+    if (TM) {
         if (warp == 0) tmem_alloc<512>(smem_u32(&tptr));
         tc_fence_before();
         __syncthreads();
@@ -186,6 +187,8 @@ __global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long*
     }
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t col0 = (warp >> 2) * 256;
+    // 16x64b: the two warps of a lane quarter take its lanes 0-15 / 16-31 (as attn11.cuh)
+    const uint32_t lane16 = (uint32_t)(32 * (warp & 3) + 16 * ((warp >> 2) & 1)) << 16;
     uint32_t acc = threadIdx.x;
     float f[8];
     for (int i = 0; i < 8; ++i) f[i] = 0.001f * (threadIdx.x + i);
@@ -214,6 +217,25 @@ __global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long*
             tmem_st32(tptr + lane_off + col0 + 32, r0);
             tmem_st32(tptr + lane_off + col0 + 64, r0);
             tmem_st32(tptr + lane_off + col0 + 96, r0);
+            tmem_wait_st();
+            acc += 1;
+        } else if (WHICH == 10) {
+            uint32_t r0[32], r1[32], r2[32], r3[32];
+            tmem_ld16x64(tptr + lane16 + 0, r0);
+            tmem_ld16x64(tptr + lane16 + 64, r1);
+            tmem_ld16x64(tptr + lane16 + 128, r2);
+            tmem_ld16x64(tptr + lane16 + 192, r3);
+            tmem_wait_ld();
+            reg_dep32(r0); reg_dep32(r1); reg_dep32(r2); reg_dep32(r3);
+            acc ^= r0[3] ^ r1[7] ^ r2[11] ^ r3[29];
+        } else if (WHICH == 11) {
+            uint32_t r0[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) r0[k] = acc + k;
+            tmem_st16x64(tptr + lane16 + 0, r0);
+            tmem_st16x64(tptr + lane16 + 64, r0);
+            tmem_st16x64(tptr + lane16 + 128, r0);
+            tmem_st16x64(tptr + lane16 + 192, r0);
             tmem_wait_st();
             acc += 1;
         } else if (WHICH == 2) {
@@ -283,7 +305,7 @@ __global__ void __launch_bounds__(256, 1) k_micro(int iters, unsigned long long*
     for (int i = 0; i < 8; ++i) s += f[i] + (float)ia[i];
     for (int i = 0; i < 4; ++i) s += (float)(x2[i] & 0xff);
     if (s == 1234.5f) sink[threadIdx.x] = s;
-    if (WHICH <= 1) {
+    if (TM) {
         tc_fence_before();
         __syncthreads();
         if (warp == 0) {
@@ -312,6 +334,8 @@ inline int run_micro(int which, int iters, double* per_clk_per_sm) {
         case 4: kern = k_micro<4>; break;
         case 5: kern = k_micro<5>; break;
         case 6: kern = k_micro<6>; break;
+        case 10: kern = k_micro<10>; break;
+        case 11: kern = k_micro<11>; break;
         default: return -1;
     }
     kern<<<sms, 256>>>(16, cyc, sink);
@@ -321,7 +345,8 @@ inline int run_micro(int which, int iters, double* per_clk_per_sm) {
     cudaFree(cyc);
     cudaFree(sink);
     const double per_iter_per_sm =
-        which >= 7 ? 256.0 * 8                      // 8 elements per thread per iteration
+        which >= 10 ? 8.0 * 32 * 128 * 4            // bytes, as 0 / 1
+      : which >= 7 ? 256.0 * 8                      // 8 elements per thread per iteration
       : which == 0 ? 8.0 * 32 * 128 * 4            // bytes: 8 warps x 32 lanes x 128 cols x 4 B
       : which == 1 ? 8.0 * 32 * 128 * 4
       : which == 2 ? 256.0 * 8

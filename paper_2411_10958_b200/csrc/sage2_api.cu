@@ -19,6 +19,7 @@
 
 #include "../../include/sage2.h"
 #include "attn10.cuh"
+#include "attn12.cuh"
 #include "attn8.cuh"
 #include "dsg.cuh"
 #include "prep.cuh"
@@ -175,7 +176,7 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10;
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12;
 constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V |
                             SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | kKernelFlags
 #ifdef SAGE2_DEV
@@ -185,14 +186,33 @@ constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SA
 
 bool flags_ok(int flags) {
     if (flags & ~kKnownFlags) return false;
-    if ((flags & kKernelFlags) == kKernelFlags) return false;
+    const int kf = flags & kKernelFlags;
+    if (kf & (kf - 1)) return false;                       // at most one kernel selector
+    // granularity ablation: v8 only; v12: kind::i8 codes only
+    if ((flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) && (flags & SAGE2_F_KERNEL_V12)) return false;
+    if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_KERNEL_V12)) return false;
     const int granf = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
     if ((flags & granf) == granf) return false;
     // granularity ablation (NEXT#4): v8 at d = 128 only, no carrier
     if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_KERNEL_V10))) return false;
-    // the E4M3 carrier holds the INT4 codes only (|c| <= 7) and exists in v8 only
+    // the E4M3 carrier holds the INT4 codes only (|c| <= 7); v8 and v11 only
     if ((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | SAGE2_F_KERNEL_V10))) return false;
     return true;
+}
+
+// Which kernel a call runs (shared by launch_prepare, launch_attention and sage2_attention_kernel: the
+// kernel fixes the order of the keys inside the V^T tile images and Delta S rows).
+int kernel_of(int N, int d, int flags) {
+    if (flags & SAGE2_F_KERNEL_V12) return 12;
+    if (flags & SAGE2_F_KERNEL_V10) return 10;
+    if (flags & SAGE2_F_KERNEL_V8) return 8;
+    // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
+    // C2-4K 648 vs 612); d = 128 non-causal N <= 8192 -> the persistent v10 (C2-1K 751 vs 718, C2-4K
+    // 1134 vs 1101); v8 elsewhere (causal, d = 128 from 16K on, the carrier / granularity variants)
+    const bool plain = !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN));
+    if (plain && d == 64) return 12;
+    if (plain && d == 128 && (N + 127) / 128 <= 64) return 10;
+    return 8;
 }
 
 template <int D>
@@ -292,15 +312,13 @@ int launch_attn10_t(AttnParams p, int B, cudaStream_t st) {
     return rc;
 }
 
-// Which kernel a call runs (shared by launch_attention and sage2_attention_kernel).
-int kernel_of(int N, int d, int flags) {
-    if (flags & SAGE2_F_KERNEL_V10) return 10;
-    if (flags & SAGE2_F_KERNEL_V8) return 8;
-    // no selector: the persistent v10 for d = 128, non-causal, N <= 8192 (C2-1K 751 vs 718 TOPS, C2-4K
-    // 1134 vs 1101); v8 elsewhere (from 16K on and for d = 64 / causal v8 is faster)
-    const bool v10 = d == 128 && !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) &&
-                     (N + 127) / 128 <= 64;
-    return v10 ? 10 : 8;
+template <bool CAUSAL, bool DUMP, bool TIMING = false>
+int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
+    constexpr uint32_t smem = Attn12Smem::ALLOC;
+    int rc = configure_smem<k_attn12<CAUSAL, DUMP, TIMING>>(smem);
+    if (rc) return rc;
+    k_attn12<CAUSAL, DUMP, TIMING><<<dim3((p.nT + 3) / 4, p.Hq, B), 640, smem, st>>>(p);
+    return cuda_rc();
 }
 
 template <int D>
@@ -310,10 +328,21 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
     const int kern = kernel_of(p.N, D, flags);
 #ifdef SAGE2_DEV
     if (flags & SAGE2_F_DEBUG_TIMING) {   // clock64 phase stamps (non-causal) into s_dump
+        if constexpr (D == 64) {
+            if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
+        }
         return kern == 10 ? launch_attn10_t<D, false, false, true>(p, B, st)
                           : launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
 #endif
+    if (kern == 12) {     // four Q tiles per CTA, b_kv = 64: head dim 64 only
+        if constexpr (D != 64) {
+            return SAGE2_EINVAL;
+        } else {
+            if (dump) return launch_attn12_t<false, true>(p, B, st);
+            return causal ? launch_attn12_t<true, false>(p, B, st) : launch_attn12_t<false, false>(p, B, st);
+        }
+    }
     if (kern == 10) {
         if (dump) return launch_attn10_t<D, false, true>(p, B, st);
         return causal ? launch_attn10_t<D, true, false>(p, B, st) : launch_attn10_t<D, false, false>(p, B, st);
@@ -611,7 +640,7 @@ int sage2_bench_mma(int kind, int iters, double* ops_per_s) {
 int sage2_microbench(int which, int iters, double* per_clk_per_sm) {
     int rc = check_device();
     if (rc) return rc;
-    if (which < 0 || which > 9 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
+    if (which < 0 || which > 11 || iters < 1 || !per_clk_per_sm) return SAGE2_EINVAL;
     return run_micro(which, iters, per_clk_per_sm);
 }
 #endif

@@ -160,19 +160,20 @@ DS_SIMT = 1024      # include/sage2.h SAGE2_F_DS_SIMT
 
 
 def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3=False, smooth_v=False,
-            gran="thread"):
-    """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`.
+            gran="thread", kernel="default"):
+    """Preprocessing kernels only (smoothing, quantization, Delta S) into `workspace`, laid out for
+    the attention kernel `kernel` will select (pass the same kernel to attention()).
 
     ds_simt=True computes Delta S with the SIMT fp32 kernel instead of the tf32 tensor-core GEMM
     (A/B checks)."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
-    fl = flags(causal, int8, qk_e4m3, smooth_v, gran) | (DS_SIMT if ds_simt else 0)
+    fl = flags(causal, int8, qk_e4m3, smooth_v, gran) | (DS_SIMT if ds_simt else 0) | KERNEL_FLAGS[kernel]
     _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096}   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096, "v12": 131072}   # include/sage2.h SAGE2_F_KERNEL_*
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
@@ -239,7 +240,8 @@ def bench_mma(kind, iters=20000):
 MICRO = {0: "tmem_ld_bytes_per_clk_sm", 1: "tmem_st_bytes_per_clk_sm", 2: "mufu_ex2_per_clk_sm",
          3: "i2f_per_clk_sm", 4: "ffma2_lanes_per_clk_sm", 5: "mma_sync_s4_ops_per_clk_sm",
          6: "mma_sync_s8_ops_per_clk_sm", 7: "f2fp_e4m3x2_elems_per_clk_sm", 8: "fmnmx3_per_clk_sm",
-         9: "softmax_mix_elems_per_clk_sm"}
+         9: "softmax_mix_elems_per_clk_sm", 10: "tmem_ld16x64_bytes_per_clk_sm",
+         11: "tmem_st16x64_bytes_per_clk_sm"}
 
 
 def microbench(which, iters=4096):
@@ -249,11 +251,11 @@ def microbench(which, iters=4096):
 
 
 def trace(out, workspace, B, Hq, Hkv, N, d, kernel="default"):
-    """clock64 phase stamps of CTA (0,0,0) (dev library): uint64 [16, 64, 16] (role, KV step, slot)."""
-    st = torch.zeros(16 * 64 * 16, dtype=torch.int64, device=out.device)
+    """clock64 phase stamps of CTA (0,0,0) (dev library): uint64 [32, 64, 16] (role, KV step, slot)."""
+    st = torch.zeros(32 * 64 * 16, dtype=torch.int64, device=out.device)
     _check(dev_lib().sage2_dev_trace(out.data_ptr(), st.data_ptr(), B, Hq, Hkv, N, d, KERNEL_FLAGS[kernel],
                                      workspace.data_ptr(), workspace.numel(), _stream()), dev_lib())
-    return st.view(16, 64, 16)
+    return st.view(32, 64, 16)
 
 
 def release_memory():

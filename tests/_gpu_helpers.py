@@ -59,3 +59,10 @@ def fp16_ulp(x):
 
 def to_np16(t):
     return t.detach().cpu().numpy().astype(np.float16)
+
+
+def kv_tile_for(N, d, causal=False, kernel="default", **flags):
+    """The b_kv of the attention kernel the library runs for these arguments (reading C-9: the
+    oracle's kv_tile must equal it): 64 for v12, 128 otherwise."""
+    from paper_2411_10958_b200 import sage2
+    return 64 if sage2.attention_kernel(N, d, causal=causal, kernel=kernel, **flags) == 12 else 128

@@ -20,6 +20,7 @@ import torch
 import oracle as orc
 from oracle import OracleConfig
 from paper_2411_10958_b200 import sage2, synth
+from tests._gpu_helpers import kv_tile_for
 from tests.test_gpu_parity import _compare_out
 
 pytestmark = pytest.mark.gpu
@@ -72,7 +73,8 @@ def test_full_size_sampled_parity(name):
         kn = k[b, hk].cpu().numpy()[None, None]
         vn = v[b, hk].cpu().numpy()[None, None]
         units = [(0, h - hk * grp, i) for i in blocks]
-        res = orc.sage2_forward_blocks(qn, kn, vn, units, OracleConfig(causal=causal), debug=True)
+        res = orc.sage2_forward_blocks(qn, kn, vn, units, OracleConfig(causal=causal, kv_tile=kv_tile_for(N, d, causal)),
+                                       debug=True)
         o_gpu = out[b, hk * grp:(hk + 1) * grp].cpu().numpy().astype(np.float64)[None]
         err, cos, worst, used, rows = _compare_out(o_gpu, res, units, N)
         print(f"{name} (b={b}, h={h}) blocks {blocks}: max|err|={err:.3e} min cos={cos:.8f} max err/bar={worst:.3f} rows beyond the bar={used}/{rows}")

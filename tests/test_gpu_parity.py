@@ -25,7 +25,7 @@ import torch
 import oracle as orc
 from oracle import OracleConfig
 from paper_2411_10958_b200 import sage2, synth
-from tests._gpu_helpers import fp16_ulp, read_prepared, region, to_np16
+from tests._gpu_helpers import fp16_ulp, kv_tile_for, read_prepared, region, to_np16
 
 pytestmark = pytest.mark.gpu
 
@@ -98,7 +98,7 @@ def test_s_int_bit_exact(N, d, kernel):
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=3)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
-    sage2.prepare(qg, kg, vg, ws)
+    sage2.prepare(qg, kg, vg, ws, kernel=kernel)
     out = torch.empty_like(qg)
     s = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, kernel=kernel)
     torch.cuda.synchronize()
@@ -119,7 +119,7 @@ def test_phat_codes(N, d, kind, kernel):
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=7)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
-    sage2.prepare(qg, kg, vg, ws)
+    sage2.prepare(qg, kg, vg, ws, kernel=kernel)
     out = torch.empty_like(qg)
     _, ph = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, with_p=True, kernel=kernel)
     torch.cuda.synchronize()
@@ -197,7 +197,8 @@ def test_output_parity(B, Hq, Hkv, N, d, causal, kind):
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     if len(units) > 40:                            # long sequences: every 9th Q block and the last
         units = units[::9] + [units[-1]]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
+                                   OracleConfig(causal=causal, kv_tile=kv_tile_for(N, d, causal)), debug=True)
     err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
     print(f"max|err|={err:.3e} min cos={cos:.8f} max err/bar={worst:.3f} rows beyond the bar "
           f"(within their certified ambiguity allowance)={used}/{rows}")
@@ -269,17 +270,20 @@ def test_accuracy_vs_fp32_attention():
         assert cs > min_cos, (kind, cs)
 
 
-@pytest.mark.parametrize("kernel,kv_tile", [("default", 128), ("v10", 128), ("v8", 128)])
+@pytest.mark.parametrize("kernel", ["default", "v10", "v8", "v12"])
 @pytest.mark.parametrize("d,causal,N", [(128, False, 384), (64, True, 384), (128, True, 300), (64, False, 200)])
-def test_kernel_variants(kernel, kv_tile, d, causal, N):
+def test_kernel_variants(kernel, d, causal, N):
     """Every attention kernel the library dispatches to matches the oracle run with its b_kv (C-9).
 
     N = 384: three Q tiles, so the two-tile kernels also run a one-tile CTA; N = 300 / 200: ragged
     last tile whose valid rows end inside a warp (the epilogue must stay warp-converged)."""
+    if kernel == "v12" and d != 64:
+        pytest.skip("v12 is the d = 64 kernel")
+    kv_tile = kv_tile_for(N, d, causal, kernel=kernel)
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=13)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
-    sage2.prepare(qg, kg, vg, ws, causal=causal)
+    sage2.prepare(qg, kg, vg, ws, causal=causal, kernel=kernel)
     out = torch.empty_like(qg)
     sage2.attention(out, ws, B, Hq, Hkv, N, d, causal=causal, kernel=kernel)
     torch.cuda.synchronize()
@@ -412,7 +416,8 @@ def test_smooth_v_output_parity(B, Hq, Hkv, N, d, causal):
     torch.cuda.synchronize()
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
     res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
-                                   OracleConfig(causal=causal, smooth_v=True), debug=True)
+                                   OracleConfig(causal=causal, smooth_v=True, kv_tile=kv_tile_for(N, d, causal)),
+                                   debug=True)
     _compare_out(to_np16(out).astype(np.float64), res, units, N)
 
 
@@ -497,7 +502,8 @@ def test_random_shapes_fuzz():
         out = sage2.attn(qg, kg, vg, causal=causal, int8=int8, smooth_v=smooth_v)
         torch.cuda.synchronize()
         units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range((N + 127) // 128)]
-        cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8)
+        cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8,
+                           kv_tile=kv_tile_for(N, d, causal))
         res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
         err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
         print(f"case {case}: B={B} Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} sv={smooth_v} "
@@ -572,3 +578,58 @@ def test_v_codes_near_e4m3_midpoints(N, d):
     kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
     assert np.array_equal(g["dv"][0].view(np.uint32), kv["dv"].view(np.uint32))
     assert np.array_equal(g["vhat"][0], kv["vhat"])
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,causal,kind,int8,smooth_v", [
+    (1, 2, 1, 256, False, "structured", False, False),       # config C1 shape, one CTA, two tiles
+    (2, 8, 2, 1000, False, "structured", False, False), (2, 8, 2, 1000, True, "iid", False, False),
+    (1, 6, 3, 777, True, "structured", False, True), (2, 4, 4, 640, False, "iid", True, False),
+    (1, 4, 1, 1, False, "iid", False, False), (1, 3, 1, 4500, True, "structured", False, False),
+    (1, 2, 2, 5000, False, "iid", False, False), (1, 2, 1, 100, True, "iid", False, False)])
+def test_v12_parity(B, Hq, Hkv, N, causal, kind, int8, smooth_v):
+    """v12 (d = 64: four Q tiles per CTA, b_kv = 64 -- the oracle runs with kv_tile = 64, reading
+    C-9) on sampled blocks over GQA, ragged N (partial 64-key steps), causal tiles of different
+    lengths inside one CTA, INT8 and smooth V."""
+    d = 64
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, kind, seed=43)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d, causal=causal)
+    sage2.prepare(qg, kg, vg, ws, causal=causal, int8=int8, smooth_v=smooth_v, kernel="v12")
+    out = torch.empty_like(qg)
+    sage2.attention(out, ws, B, Hq, Hkv, N, d, causal=causal, int8=int8, smooth_v=smooth_v, kernel="v12")
+    torch.cuda.synchronize()
+    nT = (N + 127) // 128
+    units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
+    if len(units) > 24:
+        units = units[::max(1, len(units) // 20)] + [units[-1]]
+    cfg = OracleConfig(causal=causal, smooth_v=smooth_v, qk_max=127 if int8 else 7, smooth_q=not int8, kv_tile=64)
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+    err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    print(f"v12: max|err|={err:.3e} min cos={cos:.8f} rows beyond the bar={used}/{rows}")
+
+
+@pytest.mark.parametrize("N", [256, 700, 2048])
+def test_v12_s_int_and_phat(N):
+    """S_int read back from TMEM (64-key steps) bit-exact; P^ codes equal to the kv_tile = 64 oracle's
+    except on certified-ambiguous decisions."""
+    B, Hq, Hkv, d = 1, 2, 1, 64
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=45)
+    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
+    sage2.prepare(qg, kg, vg, ws, kernel="v12")
+    out = torch.empty_like(qg)
+    s, ph = sage2.debug_qk_int32(out, ws, B, Hq, Hkv, N, d, with_p=True, kernel="v12")
+    torch.cuda.synchronize()
+    s, ph = s.cpu().numpy(), ph.cpu().numpy()
+    kv = orc.kv_head(k.numpy()[0, 0], v.numpy()[0, 0])
+    units = [(0, h, i) for h in range(Hq) for i in range((N + 127) // 128)]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(kv_tile=64), keep=True,
+                                   debug=True)
+    for u, (_, h, i) in enumerate(units):
+        qb = res["inter"][u]["qb"]
+        ref = orc.s_int_block(qb["qhat"], kv["khat"])
+        r1 = min(N, 128 * i + 128) - 128 * i
+        assert np.array_equal(s[h, 128 * i:128 * i + r1, :N].astype(np.int64), ref[:r1, :N]), (h, i)
+        dbg = res["inter"][u]["dbg"]
+        g, o = ph[h, 128 * i:128 * i + r1, :N], dbg["phat"][:r1, :N]
+        amb = dbg["amb"][:r1, :N].astype(bool)
+        assert not np.any((g != o) & ~amb)
+    _compare_out(to_np16(out).astype(np.float64), res, units, N)

@@ -15,6 +15,13 @@ import torch.multiprocessing as mp
 from paper_2411_10958_b200 import shard, synth
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -38,7 +45,7 @@ def _worker(rank, world, port, q):
 def test_two_rank_sharding():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000)
+    port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
@@ -93,7 +100,7 @@ def _strong_worker(rank, world, port, q):
 def test_two_rank_strong_split_and_gather():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 30500 + (os.getpid() % 1000)
+    port = _free_port()
     procs = [ctx.Process(target=_strong_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
