@@ -32,7 +32,7 @@ struct Attn10Smem {
     static constexpr uint32_t XM = P1 + 16384;              // float xm[2 tiles][2 buf][2 halves][128]
     static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;  // float xl[2 tiles][2 halves][128]
     static constexpr uint32_t BAR = XL + 2 * 2 * 128 * 4;
-    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 9;
+    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 11;
     static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
     static constexpr uint32_t ITEM = TMEMPTR + 16;       // int item[2]: ring of published item indices
     static constexpr uint32_t BYTES = ITEM + 16;
@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
     auto bar_r_full = [&](int k) { return bar0 + 8 * (5 + 2 * kStages2 + k); };
     auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * kStages2 + k); };
     const uint32_t bar_q_empty = bar0 + 8 * (9 + 2 * kStages2);
+    auto bar_pa_full = [&](int k) { return bar0 + 8 * (10 + 2 * kStages2 + k); };   // first halves of P^
     auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
 
     if (threadIdx.x == 0) {
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
         for (int k = 0; k < 2; ++k) {
             mbar_init(bar_s_full(k), 1);
             mbar_init(bar_p_full(k), 256);
+            mbar_init(bar_pa_full(k), 256);
             mbar_init(bar_r_full(k), 1);
             mbar_init(bar_s_free(k), 256);
         }
@@ -212,11 +214,23 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                         else mma_i8_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
                     }
                     mma_commit_w(bar_s_full(k));
-                    mbar_wait(bar_p_full(k), tph);                      // softmax_k wrote P^_k
-                    tc_fence_after();
                     const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
+                    if (SAGE2_PSPLIT) {
+                        // as v8: K steps 0 and 2 (each key half's first 32 codes) first, then 1 and 3
+                        mbar_wait(bar_pa_full(k), tph);
+                        tc_fence_after();
+                        mma_f8f6f4_w(tS, pdesc + 0, vdesc + 0, IDPV, 0);
+                        mma_f8f6f4_w(tS, pdesc + 4, vdesc + 4, IDPV, 1);
+                        mbar_wait(bar_p_full(k), tph);                  // softmax_k wrote all of P^_k
+                        tc_fence_after();
+                        mma_f8f6f4_w(tS, pdesc + 2, vdesc + 2, IDPV, 1);
+                        mma_f8f6f4_w(tS, pdesc + 6, vdesc + 6, IDPV, 1);
+                    } else {
+                        mbar_wait(bar_p_full(k), tph);                  // softmax_k wrote P^_k
+                        tc_fence_after();
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                        for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                    }
                     mma_commit_w(bar_r_full(k));
                     mma_commit_w(bar_kv_empty(s));
                     tph ^= 1u;
@@ -368,6 +382,11 @@ __global__ void __launch_bounds__(640, 1) k_attn10(const AttnParams p, int nitem
                     if (DUMP && p.p_dump)
                         *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h + c0) =
                             make_uint4(w[0], w[1], w[2], w[3]);
+                    if (SAGE2_PSPLIT && c0 == 16) {                  // this half's first 32 codes are in smem
+                        fence_proxy_async_smem();
+                        tc_fence_before();
+                        mbar_arrive(bar_pa_full(k));
+                    }
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();

@@ -32,10 +32,6 @@
 
 namespace sage2 {
 
-#ifndef SAGE2_PSPLIT
-#define SAGE2_PSPLIT 1   // hand P^ to the PV MMA in two halves (A/B builds: 0 = one hand-off per tile)
-#endif
-
 template <int D>
 struct Attn8Smem {
     using B2 = PairSmem<D>;

@@ -4,6 +4,10 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#ifndef SAGE2_PSPLIT
+#define SAGE2_PSPLIT 1   // v8/v10: hand P^ to the PV MMA in two halves (A/B builds: 0 = one hand-off per tile)
+#endif
+
 namespace sage2 {
 
 struct AttnParams {
