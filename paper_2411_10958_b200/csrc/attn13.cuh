@@ -1,0 +1,457 @@
+// attn13.cuh -- SageAttention2 attention kernel v13 for sm_100a (Alg. 1 inner loop, PAPER.md:246-263;
+// b_kv = 128): v8's CTA (two 128-row Q tiles, 16 softmax warps split by key halves, exact max
+// exchange, MUFU turns alternating between the tiles) with the S of the NEXT key tile computed while
+// the current one is exponentiated.
+//
+// v8's critical path: S_k and R_k share TMEM columns, so QK(j+1) could only be issued once R(j) had
+// been read and promoted; the post-exp chain PV(j) -> R read -> promotion -> QK(j+1) -> S load ->
+// dequant -> max exchange (~2000 cycles) outlasted the other tile's exp phase (~1024), and the MUFU
+// idled.  v13 keeps the same TMEM plan (S_k/R_k in one 128-column region, O_k in another: both tiles
+// use all 512 columns) but reorders the region's use per tile k:
+//
+//     QK(j+1) -> X   is issued as soon as R(j-1) has been read out of X (during the previous
+//                    non-exp phase), so it runs under exp(j);
+//     after exp(j):  the softmax warps load S(j+1) out of X into registers (X free again), then
+//     PV(j) -> X     (fresh R) runs while the warps dequantize S(j+1) and take its partial
+//                    row max;
+//     promotion      O = alpha_j O + R(j) in 16-column chunks with S(j+1) held
+//                    in registers; reading R(j) frees X for QK(j+2).
+//
+// The non-exp chain is now S load -> dequant -> promotion -> max exchange, with both MMAs of the
+// tile off it.  Arithmetic is exactly v8's (same dequant, same max, same exp, same P^, same PV K-step
+// order, same promotion), so v13's output is bitwise v8's.
+//
+// Warp roles (640 threads): warp 0 producer (bulk-async copies of the pre-swizzled tile images into a
+// KS-deep ring), warps 1/2 MMA issuers of tile 0/1, warp 3 idle, warps 4 + 8k + 4h + {0..3} softmax of
+// Q tile k, key half h (one thread per (row, half); TMEM lane = row).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "prep.cuh"
+#include "ptx.cuh"
+
+namespace sage2 {
+
+#ifndef SAGE2_KSTAGES13
+#define SAGE2_KSTAGES13 4
+#endif
+
+#ifndef SAGE2_PC13
+#define SAGE2_PC13 8
+#endif
+constexpr int PC = SAGE2_PC13;   // promotion chunk (TMEM columns per load): S(j+1) stays in registers meanwhile
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t a, uint32_t (&r)[N]) {
+    if constexpr (N == 8) tmem_ld8(a, r); else if constexpr (N == 16) tmem_ld16(a, r); else tmem_ld32(a, r);
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t a, const uint32_t (&r)[N]) {
+    if constexpr (N == 8) tmem_st8(a, r); else if constexpr (N == 16) tmem_st16(a, r); else tmem_st32(a, r);
+}
+template <int N>
+__device__ __forceinline__ void reg_depn(uint32_t (&r)[N]) {
+    if constexpr (N == 8) reg_dep8(r); else if constexpr (N == 16) reg_dep16(r); else reg_dep32(r);
+}
+
+template <int D>
+struct Attn13Smem {
+    static constexpr int KS = SAGE2_KSTAGES13;             // K/V ring depth (QK runs a tile ahead)
+    static constexpr uint32_t TILE = 128 * D;
+    static constexpr uint32_t Q0 = 0, Q1 = TILE;
+    static constexpr uint32_t ST_K = 0, ST_V = TILE, ST_DS0 = 2 * TILE, ST_DS1 = 2 * TILE + 512,
+                              ST_DK = 2 * TILE + 1024;
+    static constexpr uint32_t STAGE = ((2 * TILE + 1024 + 512) + 1023) / 1024 * 1024;
+    static constexpr uint32_t ST0 = 2 * TILE;
+    static constexpr uint32_t P0 = ST0 + KS * STAGE, P1 = P0 + 16384;
+    static constexpr uint32_t XM = P1 + 16384;                // float xm[2 tiles][2 buf][2 halves][128]
+    static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;  // float xl[2 tiles][2 halves][128]
+    static constexpr uint32_t BAR = XL + 2 * 2 * 128 * 4;
+    static constexpr uint32_t NBAR = 1 + 2 * KS + 12;
+    static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
+    static constexpr uint32_t BYTES = TMEMPTR + 16;
+    static constexpr uint32_t ALLOC = BYTES + 1024;
+};
+
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
+__global__ void __launch_bounds__(640, 1) k_attn13(const AttnParams p) {
+    using L = Attn13Smem<D>;
+    constexpr int KS = L::KS;
+    constexpr int DH = D / 2;                      // output channels per half
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
+
+    const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+    const int wg = warp / 4;
+    const int nT = p.nT, Np = nT * 128;
+    const int npairs = (nT + 1) / 2;
+    const int pair = CAUSAL ? (npairs - 1 - (int)blockIdx.x) : (int)blockIdx.x;   // heavy causal pairs first
+    const int hq = blockIdx.y, b = blockIdx.z;
+    const int bhq = b * p.Hq + hq;
+    const int bhk = b * p.Hkv + hq / (p.Hq / p.Hkv);
+    const int it0 = 2 * pair, it1 = 2 * pair + 1;
+    const int nkv0 = CAUSAL ? it0 + 1 : nT;
+    const int nkv1 = (it1 < nT) ? (CAUSAL ? it1 + 1 : nT) : 0;
+    const int nkv_max = nkv0 > nkv1 ? nkv0 : nkv1;
+    const int ntiles = nkv1 > 0 ? 2 : 1;
+
+    auto s_as_float = [](uint32_t u) { return QKF8 ? __uint_as_float(u) : (float)(int32_t)u; };
+    auto s_as_int = [](uint32_t u) { return QKF8 ? (int32_t)__uint_as_float(u) : (int32_t)u; };
+    const bool tsel = TIMING && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    auto ts = [&](int who, int j, int slot) {
+        if (TIMING && tsel && j < 64)
+            reinterpret_cast<unsigned long long*>(p.s_dump)[(who * 64 + j) * 16 + slot] = clock64();
+    };
+    const uint32_t bar0 = sbase + L::BAR;
+    const uint32_t bar_q = bar0;
+    auto bar_kv_full = [&](int s) { return bar0 + 8 * (1 + s); };
+    auto bar_kv_empty = [&](int s) { return bar0 + 8 * (1 + KS + s); };
+    auto bar_s_full = [&](int k) { return bar0 + 8 * (1 + 2 * KS + k); };    // QK(j) in X_k
+    auto bar_s_read = [&](int k) { return bar0 + 8 * (3 + 2 * KS + k); };    // S(j) read out of X_k
+    auto bar_pa_full = [&](int k) { return bar0 + 8 * (5 + 2 * KS + k); };   // first halves of P^
+    auto bar_p_full = [&](int k) { return bar0 + 8 * (7 + 2 * KS + k); };    // all of P^
+    auto bar_r_full = [&](int k) { return bar0 + 8 * (9 + 2 * KS + k); };    // R(j) in X_k
+    auto bar_r_free = [&](int k) { return bar0 + 8 * (11 + 2 * KS + k); };   // R(j) read out of X_k
+    auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < KS; ++s) {
+            mbar_init(bar_kv_full(s), 1);
+            mbar_init(bar_kv_empty(s), 2);      // one arrival per Q tile (MMA commit or bypass)
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(bar_s_full(k), 1);
+            mbar_init(bar_s_read(k), 256);
+            mbar_init(bar_pa_full(k), 256);
+            mbar_init(bar_p_full(k), 256);
+            mbar_init(bar_r_full(k), 1);
+            mbar_init(bar_r_free(k), 256);
+        }
+        fence_mbar_init();
+    }
+    constexpr int CW = 0, SW0 = 1;
+    if (warp == 4 * CW) tmem_alloc<512>(sbase + L::TMEMPTR);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(sgen + L::TMEMPTR);
+
+    if (wg == CW) {
+        setmaxnreg_dec<32>();
+        if (warp == 4 * CW && lane == 0) {
+            // ===================== producer =====================
+            const size_t tile_bytes = (size_t)128 * D;
+            mbar_arrive_expect_tx(bar_q, L::TILE * ntiles);
+            bulk_g2s(sbase + L::Q0, p.qhat + ((size_t)bhq * nT + it0) * tile_bytes, L::TILE, bar_q);
+            if (ntiles == 2)
+                bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)bhq * nT + it1) * tile_bytes, L::TILE, bar_q);
+            const uint64_t keep = policy_evict_last();
+            for (int j = 0; j < nkv_max; ++j) {
+                const int s = j % KS;
+                if (j >= KS) mbar_wait(bar_kv_empty(s), ((j / KS) - 1) & 1);
+                const uint32_t sa = stage_addr(s);
+                const bool d0 = j < nkv0, d1 = j < nkv1;
+                constexpr int NGK = gran_nk(GRAN);
+                mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 4 * NGK + 512 * (d0 + d1));
+                bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+                bulk_g2s(sa + L::ST_DK, p.dk + ((size_t)bhk * nT + j) * NGK, 4 * NGK, bar_kv_full(s));
+                if (d0)
+                    bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+                if (d1)
+                    bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, bhq, it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+            }
+        } else if (warp == 4 * CW + 1 || warp == 4 * CW + 2) {
+            // ============ MMA issuer for Q tile k (whole warp converged, one elected lane issues) ============
+            const int k = warp - (4 * CW + 1);
+            const int my_nkv = k ? nkv1 : nkv0;
+            constexpr uint32_t IDQK = QKF8 ? idesc_e4m3(128, 128) : idesc_i8(128, 128);
+            constexpr uint32_t IDPV = idesc_e4m3(128, D);
+            const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
+            const uint64_t pdesc = smem_desc<128>(sbase + (k ? L::P1 : L::P0));
+            const uint32_t tX = tmem + 128 * k;
+            auto issue_qk = [&](int jj) {
+                const int s = jj % KS;
+                mbar_wait(bar_kv_full(s), (jj / KS) & 1);
+                tc_fence_after();
+                const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K);
+#pragma unroll
+                for (int kk = 0; kk < D / 32; ++kk) {
+                    if (QKF8) mma_f8f6f4_w(tX, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                    else mma_i8_w(tX, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                }
+                mma_commit_w(bar_s_full(k));
+            };
+            mbar_wait(bar_q, 0);
+            if (my_nkv > 0) issue_qk(0);
+            if (my_nkv > 1) {
+                mbar_wait(bar_s_read(k), 0);                  // S(0) read out of X
+                issue_qk(1);
+            }
+            for (int j = 0; j < my_nkv; ++j) {
+                const int s = j % KS;
+                const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
+                // each key half's first 32 codes (P^ columns 0-31 and 64-95: K steps 0 and 2) are
+                // multiplied while the softmax still exponentiates the second 32 (v8's order)
+                mbar_wait(bar_pa_full(k), j & 1);
+                if (j + 1 < my_nkv) mbar_wait(bar_s_read(k), (j + 1) & 1);   // S(j+1) read out of X
+                if (lane == 0) ts(2 + k, j, 3);
+                tc_fence_after();
+                mma_f8f6f4_w(tX, pdesc + 0, vdesc + 0, IDPV, 0);
+                mma_f8f6f4_w(tX, pdesc + 4, vdesc + 4, IDPV, 1);
+                mbar_wait(bar_p_full(k), j & 1);                    // softmax_k(j) wrote all of P^_k
+                tc_fence_after();
+                mma_f8f6f4_w(tX, pdesc + 2, vdesc + 2, IDPV, 1);
+                mma_f8f6f4_w(tX, pdesc + 6, vdesc + 6, IDPV, 1);
+                mma_commit_w(bar_r_full(k));
+                mma_commit_w(bar_kv_empty(s));                      // K(j) and V(j) consumed
+                if (lane == 0) ts(2 + k, j, 4);
+                if (j + 2 < my_nkv) {
+                    mbar_wait(bar_r_free(k), j & 1);                // R(j) read out of X
+                    if (lane == 0) ts(2 + k, j, 5);
+                    issue_qk(j + 2);
+                    if (lane == 0) ts(2 + k, j, 6);
+                }
+            }
+            for (int j = my_nkv; j < nkv_max; ++j) {                // stages only the other tile uses
+                const int s = j % KS;
+                mbar_wait(bar_kv_full(s), (j / KS) & 1);
+                if (lane == 0) mbar_arrive(bar_kv_empty(s));
+            }
+        }
+    } else {
+        setmaxnreg_inc<112>();      // pool = 96 x 640 (launch): 32 + 4 x 112 = 5 x 96
+        // ============ softmax (key half h) + two-level promotion + epilogue for Q tile k ============
+        const int k = (wg - SW0) >> 1, h = (wg - SW0) & 1;
+        const int my_nkv = k ? nkv1 : nkv0, my_it = k ? it1 : it0;
+        auto turn_wait = [&]() { named_bar_sync(1 + k, 512); };
+        auto turn_pass = [&]() { named_bar_arrive(1 + (1 - k), 512); };
+        auto pair_sync = [&]() { named_bar_sync(3 + k, 256); };   // the two halves of tile k
+        if (k == 1) turn_pass();                    // tile 0 takes the first MUFU turn
+        if (my_nkv > 0) {
+            const int wq = warp & 3;
+            const int row = 32 * wq + lane;
+            const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+            const uint32_t tS = tmem + 128 * k + lane_off + 64 * h;      // this half's S columns
+            const uint32_t tR = tmem + 128 * k + lane_off + DH * h;      // this half's R channels
+            const uint32_t tO = tmem + 256 + D * k + lane_off + DH * h;  // this half's O channels
+            const int grow = my_it * 128 + row;
+            const float dqr = p.dq[((size_t)bhq * nT + my_it) * gran_nq(GRAN) +
+                                   (GRAN == 2 ? row : GRAN == 1 ? 0 : 8 * (row / 32) + (row % 8))] * p.qk_scale_log2;
+            uint8_t* sP = sgen + (k ? L::P1 : L::P0);
+            float* xm = reinterpret_cast<float*>(sgen + L::XM) + k * 512;    // [buf][half][128]
+            float m = -INFINITY, l = 0.0f;
+            const bool tme = TIMING && h == 0 && row == 0;
+            auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
+            float sv[64];
+            float mh;
+            // S(jj) out of X (then X is free for PV(jj-1)), dequantized + Delta S, masked (C-18),
+            // and this half's row max
+            auto load_s = [&](int jj) {
+                const int s = jj % KS;
+                mbar_wait(bar_kv_full(s), (jj / KS) & 1);        // Delta S / delta_K landed
+                mbar_wait(bar_s_full(k), jj & 1);
+                tc_fence_after();
+                if (jj > 0) tss(jj - 1, 1);
+                const uint32_t dss = stage_addr(s) + (k ? L::ST_DS1 : L::ST_DS0) + 256 * h;
+                const float* dks = reinterpret_cast<const float*>(sgen + L::ST0 + s * L::STAGE + L::ST_DK) +
+                                   (GRAN == 1 ? h : 4 * h);
+                const uint32_t dkv = stage_addr(s) + L::ST_DK + 256 * h;   // per-token delta_K of this half
+                float2 sc2[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float v = dqr * dks[GRAN == 1 ? 0 : g];
+                    sc2[g] = make_float2(v, v);
+                }
+                const float2 dq2 = make_float2(dqr, dqr);
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tS + 0, r0);
+                tmem_ld32(tS + 32, r1);
+                tmem_wait_ld();
+                reg_dep32(r0);
+                reg_dep32(r1);
+                tc_fence_before();
+                mbar_arrive(bar_s_read(k));                     // X free: PV(jj-1) may write R
+                if (jj > 0) tss(jj - 1, 9);
+                if (DUMP) {
+                    int32_t* dst = p.s_dump + ((size_t)bhq * Np + grow) * (size_t)Np + jj * 128 + 64 * h;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        dst[c] = s_as_int(r0[c]);
+                        dst[32 + c] = s_as_int(r1[c]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 64; c += 4) {
+                    const uint32_t* rr = c < 32 ? r0 : r1;
+                    const float4 d4 = lds128(dss + 4 * c);
+                    const int g = (c % 8) / 2;
+                    float2 sa2 = sc2[g], sb2 = sc2[g + 1];
+                    if (GRAN == 2) {                     // one delta_K per key column
+                        const float4 k4 = lds128(dkv + 4 * c);
+                        sa2 = fmul2(make_float2(k4.x, k4.y), dq2);
+                        sb2 = fmul2(make_float2(k4.z, k4.w), dq2);
+                    }
+                    const float2 a = ffma2(make_float2(s_as_float(rr[c % 32]), s_as_float(rr[c % 32 + 1])),
+                                           sa2, make_float2(d4.x, d4.y));
+                    const float2 bq = ffma2(make_float2(s_as_float(rr[c % 32 + 2]), s_as_float(rr[c % 32 + 3])),
+                                            sb2, make_float2(d4.z, d4.w));
+                    sv[c] = a.x;
+                    sv[c + 1] = a.y;
+                    sv[c + 2] = bq.x;
+                    sv[c + 3] = bq.y;
+                }
+                if ((CAUSAL && jj == my_it) || (jj * 128 + 128 > p.N)) {   // C-18
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) {
+                        const int key = jj * 128 + 64 * h + c;
+                        if (key >= p.N || (CAUSAL && key > grow)) sv[c] = -INFINITY;
+                    }
+                }
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int c = 0; c < 64; c += 8) {
+                    mx[0] = fmax3(mx[0], sv[c], sv[c + 1]);
+                    mx[1] = fmax3(mx[1], sv[c + 2], sv[c + 3]);
+                    mx[2] = fmax3(mx[2], sv[c + 4], sv[c + 5]);
+                    mx[3] = fmax3(mx[3], sv[c + 6], sv[c + 7]);
+                }
+                mh = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
+            };
+            load_s(0);
+            for (int j = 0; j < my_nkv; ++j) {
+                tss(j, 2);
+                // exact row max over both halves (C-10): exchange through shared memory
+                float* xmb = xm + (j & 1) * 256;
+                xmb[h * 128 + row] = mh;
+                pair_sync();
+                const float m_new = fmax3(m, mh, xmb[(1 - h) * 128 + row]);
+                const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
+                const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
+                tss(j, 3);
+                turn_wait();
+                tss(j, 4);
+                const float2 negm = make_float2(-m_use, -m_use);
+                float2 rs2 = make_float2(0.f, 0.f), rs2b = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 16) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c0 + 4 * q;
+                        const float2 x01 = fadd2(make_float2(sv[c], sv[c + 1]), negm);
+                        const float2 x23 = fadd2(make_float2(sv[c + 2], sv[c + 3]), negm);
+                        const float2 p01 = make_float2(ex2_approx(x01.x), ex2_approx(x01.y));
+                        const float2 p23 = make_float2(ex2_approx(x23.x), ex2_approx(x23.y));
+                        rs2 = fadd2(rs2, p01);
+                        rs2b = fadd2(rs2b, p23);
+                        const uint32_t lo = __nv_cvt_float2_to_fp8x2(p01, __NV_SATFINITE, __NV_E4M3);
+                        const uint32_t hi = __nv_cvt_float2_to_fp8x2(p23, __NV_SATFINITE, __NV_E4M3);
+                        w[q] = lo | (hi << 16);
+                    }
+                    *reinterpret_cast<uint4*>(sP + swz_off<128>(row, 64 * h + c0)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    if (DUMP && p.p_dump)
+                        *reinterpret_cast<uint4*>(p.p_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h + c0) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
+                    if (c0 == 16) {                                  // this half's first 32 codes are in smem
+                        fence_proxy_async_smem();
+                        tc_fence_before();
+                        mbar_arrive(bar_pa_full(k));
+                    }
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(bar_p_full(k));
+                tss(j, 5);
+                turn_pass();
+                l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
+                m = m_new;
+                if (j + 1 < my_nkv) load_s(j + 1);                  // S(j+1): computed under exp(j)
+                tss(j, 6);
+                // ---- two-level promotion O = alpha * O + R(j), 16 channels at a time ----
+                mbar_wait(bar_r_full(k), j & 1);
+                tc_fence_after();
+                tss(j, 7);
+                const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+                for (int c0 = 0; c0 < DH; c0 += PC) {
+                    uint32_t r[PC], o[PC];
+                    tmem_ldn(tR + c0, r);
+                    if (j > 0) tmem_ldn(tO + c0, o);
+                    tmem_wait_ld();
+                    reg_depn(r);
+                    if (j > 0) {
+                        reg_depn(o);
+#pragma unroll
+                        for (int c = 0; c < PC; c += 2) {
+                            const float2 v = ffma2(a2, make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])),
+                                                   make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
+                            o[c] = __float_as_uint(v.x);
+                            o[c + 1] = __float_as_uint(v.y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < PC; ++c) o[c] = r[c];
+                    }
+                    tmem_stn(tO + c0, o);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(bar_r_free(k));                // X free: QK(j+2) may overwrite it
+                tss(j, 8);
+            }
+            // ---- epilogue: O / (l_0 + l_1) / 448 * delta_V  (l carries the 448 factor) ----
+            float* xl = reinterpret_cast<float*>(sgen + L::XL) + k * 256;
+            xl[h * 128 + row] = l;
+            pair_sync();
+            const float inv_l = 1.0f / (xl[row] + xl[128 + row]);
+            const float* dvp = p.dv + (size_t)bhk * D + DH * h;
+            const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D + DH * h : nullptr;   // smooth V: O + V_m
+            __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D + DH * h;
+#pragma unroll
+            for (int c0 = 0; c0 < DH; c0 += 32) {
+                uint32_t o[32];
+                tmem_ld32(tO + c0, o);
+                tmem_wait_ld();
+                reg_dep32(o);
+                if (grow < p.N) {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 8) {
+                        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c));
+                        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c + 4));
+                        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 m0 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c)) : z;
+                        const float4 m1 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c + 4)) : z;
+                        __half2 h0 = __floats2half2_rn(fmaf(__uint_as_float(o[c]) * inv_l, d0.x, m0.x),
+                                                       fmaf(__uint_as_float(o[c + 1]) * inv_l, d0.y, m0.y));
+                        __half2 h1 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 2]) * inv_l, d0.z, m0.z),
+                                                       fmaf(__uint_as_float(o[c + 3]) * inv_l, d0.w, m0.w));
+                        __half2 h2 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 4]) * inv_l, d1.x, m1.x),
+                                                       fmaf(__uint_as_float(o[c + 5]) * inv_l, d1.y, m1.y));
+                        __half2 h3 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 6]) * inv_l, d1.z, m1.z),
+                                                       fmaf(__uint_as_float(o[c + 7]) * inv_l, d1.w, m1.w));
+                        *reinterpret_cast<uint4*>(orow + c0 + c) =
+                            make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                       *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+                    }
+                }
+            }
+        }
+        for (int j = my_nkv; j < nkv_max; ++j) {    // keep the MUFU turn protocol balanced
+            turn_wait();
+            turn_pass();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4 * CW) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+}  // namespace sage2

@@ -20,6 +20,7 @@
 #include "../../include/sage2.h"
 #include "attn10.cuh"
 #include "attn12.cuh"
+#include "attn13.cuh"
 #include "attn8.cuh"
 #include "dsg.cuh"
 #include "prep.cuh"
@@ -176,7 +177,7 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12;
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12 | SAGE2_F_KERNEL_V13;
 constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V |
                             SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | kKernelFlags
 #ifdef SAGE2_DEV
@@ -206,6 +207,7 @@ int kernel_of(int N, int d, int flags) {
     if (flags & SAGE2_F_KERNEL_V12) return 12;
     if (flags & SAGE2_F_KERNEL_V10) return 10;
     if (flags & SAGE2_F_KERNEL_V8) return 8;
+    if (flags & SAGE2_F_KERNEL_V13) return 13;
     // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
     // C2-4K 648 vs 612); d = 128 non-causal N <= 8192 -> the persistent v10 (C2-1K 751 vs 718, C2-4K
     // 1134 vs 1101); v8 elsewhere (causal, d = 128 from 16K on, the carrier / granularity variants)
@@ -312,6 +314,15 @@ int launch_attn10_t(AttnParams p, int B, cudaStream_t st) {
     return rc;
 }
 
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
+int launch_attn13_t(const AttnParams& p, int B, cudaStream_t st) {
+    constexpr uint32_t smem = Attn13Smem<D>::ALLOC;
+    int rc = configure_smem<k_attn13<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>>(smem);
+    if (rc) return rc;
+    k_attn13<D, CAUSAL, DUMP, QKF8, TIMING, GRAN><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
+    return cuda_rc();
+}
+
 template <bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn12Smem::ALLOC;
@@ -331,6 +342,7 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if constexpr (D == 64) {
             if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
         }
+        if (kern == 13) return launch_attn13_t<D, false, false, false, true>(p, B, st);
         return kern == 10 ? launch_attn10_t<D, false, false, true>(p, B, st)
                           : launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
@@ -346,6 +358,12 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
     if (kern == 10) {
         if (dump) return launch_attn10_t<D, false, true>(p, B, st);
         return causal ? launch_attn10_t<D, true, false>(p, B, st) : launch_attn10_t<D, false, false>(p, B, st);
+    }
+    if (kern == 13) {
+        if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) return SAGE2_EINVAL;
+        if (dump) return f8 ? launch_attn13_t<D, false, true, true>(p, B, st) : launch_attn13_t<D, false, true>(p, B, st);
+        if (f8) return causal ? launch_attn13_t<D, true, false, true>(p, B, st) : launch_attn13_t<D, false, false, true>(p, B, st);
+        return causal ? launch_attn13_t<D, true, false>(p, B, st) : launch_attn13_t<D, false, false>(p, B, st);
     }
     if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
         if constexpr (D != 128) {
