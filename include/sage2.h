@@ -67,8 +67,9 @@ extern "C" {
 #define SAGE2_F_KERNEL_V12 131072 /* force the v12 kernel (csrc/attn12.cuh, d = 64 only: four Q tiles per  */
                                   /* CTA, b_kv = 64 -- the oracle's kv_tile is then 64, reading C-9).      */
                                   /* Not with QK_E4M3 / GRAN flags.                                       */
-#define SAGE2_F_KERNEL_V13 1048576 /* force the v13 kernel (csrc/attn13.cuh: v8's CTA with QK of the next   */
-                                  /* key tile issued under the current exp; bitwise v8's output)          */
+#define SAGE2_F_ONE_LEVEL 1048576 /* ablation of the two-level accumulation (Table): the  */
+                                  /* PV MMA accumulates into O in TMEM (O rescaled in place where the row */
+                                  /* max moved); kernel v8 only.  Not the SageAttn2 default.              */
 #define SAGE2_F_SMOOTH_V 32768    /* optional smooth V (NEXT#2): V' = V - V_m before the       */
                                   /* per-channel FP8 quantization, O + V_m in the epilogue                */
 #define SAGE2_F_GRAN_BLOCK 262144 /* NEXT#4 ablation: per-block Q/K quantization groups (Q: 128-token     */

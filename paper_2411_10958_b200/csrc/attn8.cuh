@@ -51,7 +51,11 @@ struct Attn8Smem {
 
 // GRAN: Q/K quantization granularity of the NEXT#4 ablation (0 per-thread = SageAttn2, 1 per-block,
 // 2 per-token; prep.cuh gran_nq / gran_nk give the stored scales per 128 tokens).
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
+// ONE: single-level accumulation ablation (P:1082 row "+ Two-level accumulation"; oracle two_level =
+// false): the PV MMA accumulates straight into O in TMEM (enable-input-D after the first key tile),
+// O is rescaled in place only in rows whose running max moved (alpha = 1 exactly otherwise), and S_k
+// no longer shares its TMEM columns with R_k, so QK(j+1) is issued as soon as S(j) is in registers.
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false>
 __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     using L = Attn8Smem<D>;
     constexpr int DH = D / 2;                      // output channels per half
@@ -154,6 +158,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
             const uint64_t pdesc = smem_desc<128>(sbase + (k ? L::P1 : L::P0));
             const uint32_t tS = tmem + 128 * k;
+            const uint32_t tPV = ONE ? tmem + 256 + D * k : tS;   // R over S (two-level) or O itself (ONE)
             mbar_wait(bar_q, 0);
             for (int j = 0; j < nkv_max; ++j) {
                 const int s = j % kStages2;
@@ -181,18 +186,18 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                     mbar_wait(bar_pa_full(k), j & 1);
                     if (lane == 0) ts(2 + k, j, 3);
                     tc_fence_after();
-                    mma_f8f6f4_w(tS, pdesc + 0, vdesc + 0, IDPV, 0);
-                    mma_f8f6f4_w(tS, pdesc + 4, vdesc + 4, IDPV, 1);
+                    mma_f8f6f4_w(tPV, pdesc + 0, vdesc + 0, IDPV, ONE && j > 0);
+                    mma_f8f6f4_w(tPV, pdesc + 4, vdesc + 4, IDPV, 1);
                     mbar_wait(bar_p_full(k), j & 1);                // softmax_k(j) wrote all of P^_k
                     tc_fence_after();
-                    mma_f8f6f4_w(tS, pdesc + 2, vdesc + 2, IDPV, 1);
-                    mma_f8f6f4_w(tS, pdesc + 6, vdesc + 6, IDPV, 1);
+                    mma_f8f6f4_w(tPV, pdesc + 2, vdesc + 2, IDPV, 1);
+                    mma_f8f6f4_w(tPV, pdesc + 6, vdesc + 6, IDPV, 1);
                 } else {
                     mbar_wait(bar_p_full(k), j & 1);                // softmax_k(j) wrote P^_k
                     if (lane == 0) ts(2 + k, j, 3);
                     tc_fence_after();
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tS, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0);
+                    for (int kk = 0; kk < 4; ++kk) mma_f8f6f4_w(tPV, pdesc + 2 * kk, vdesc + 2 * kk, IDPV, kk > 0 || (ONE && j > 0));
                 }
                 mma_commit_w(bar_r_full(k));
                 mma_commit_w(bar_kv_empty(s));
@@ -249,6 +254,10 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                     tmem_wait_ld();
                     reg_dep32(r0);
                     reg_dep32(r1);
+                    if (ONE) {                                  // S in registers: QK(j+1) may overwrite it
+                        tc_fence_before();
+                        mbar_arrive(bar_s_free(k));
+                    }
                     tss(j, 9);
                     if (DUMP) {
                         int32_t* dst = p.s_dump + ((size_t)bhq * Np + grow) * (size_t)Np + j * 128 + 64 * h;
@@ -304,6 +313,31 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
                 const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
                 tss(j, 3);
+                if (ONE && j > 0) {
+                    // PV(j-1) has finished reading P^ and accumulating into O; rows whose max moved
+                    // get O *= alpha before PV(j) accumulates (alpha is exactly 1 in the others)
+                    mbar_wait(bar_r_full(k), (j - 1) & 1);
+                    tc_fence_after();
+                    if (__any_sync(0xffffffffu, m_new != m)) {
+                        const float f = (m_new != m) ? alpha : 1.0f;
+                        const float2 f2 = make_float2(f, f);
+#pragma unroll
+                        for (int c0 = 0; c0 < DH; c0 += 8) {     // S(j) stays live: 8 columns at a time
+                            uint32_t o[8];
+                            tmem_ld8(tO + c0, o);
+                            tmem_wait_ld();
+                            reg_dep8(o);
+#pragma unroll
+                            for (int c = 0; c < 8; c += 2) {
+                                const float2 v = fmul2(f2, make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])));
+                                o[c] = __float_as_uint(v.x);
+                                o[c + 1] = __float_as_uint(v.y);
+                            }
+                            tmem_st8(tO + c0, o);
+                        }
+                        tmem_wait_st();
+                    }
+                }
                 turn_wait();
                 tss(j, 4);
                 const float2 negm = make_float2(-m_use, -m_use);
@@ -341,6 +375,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 turn_pass();
                 l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
                 m = m_new;
+                if (ONE) continue;
                 // ---- two-level promotion O = alpha * O + R(j) ----
                 mbar_wait(bar_r_full(k), j & 1);
                 tc_fence_after();
@@ -378,6 +413,10 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 }
                 tmem_wait_st();
                 tss(j, 8);
+            }
+            if (ONE) {                                      // the last PV has accumulated into O
+                mbar_wait(bar_r_full(k), (my_nkv - 1) & 1);
+                tc_fence_after();
             }
             // ---- epilogue: O / (l_0 + l_1) / 448 * delta_V  (l carries the 448 factor) ----
             float* xl = reinterpret_cast<float*>(sgen + L::XL) + k * 256;

@@ -20,7 +20,6 @@
 #include "../../include/sage2.h"
 #include "attn10.cuh"
 #include "attn12.cuh"
-#include "attn13.cuh"
 #include "attn8.cuh"
 #include "dsg.cuh"
 #include "prep.cuh"
@@ -177,8 +176,8 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12 | SAGE2_F_KERNEL_V13;
-constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V |
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12;
+constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V | SAGE2_F_ONE_LEVEL |
                             SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | kKernelFlags
 #ifdef SAGE2_DEV
                             | SAGE2_F_DEBUG_TIMING
@@ -194,6 +193,8 @@ bool flags_ok(int flags) {
     if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_KERNEL_V12)) return false;
     const int granf = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
     if ((flags & granf) == granf) return false;
+    // single-level ablation: v8 only, per-thread granularity
+    if ((flags & SAGE2_F_ONE_LEVEL) && (flags & (granf | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12))) return false;
     // granularity ablation (NEXT#4): v8 at d = 128 only, no carrier
     if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_KERNEL_V10))) return false;
     // the E4M3 carrier holds the INT4 codes only (|c| <= 7); v8 and v11 only
@@ -206,14 +207,13 @@ bool flags_ok(int flags) {
 int kernel_of(int N, int d, int flags) {
     if (flags & SAGE2_F_KERNEL_V12) return 12;
     if (flags & SAGE2_F_KERNEL_V10) return 10;
-    if (flags & SAGE2_F_KERNEL_V8) return 8;
-    if (flags & SAGE2_F_KERNEL_V13) return 13;
+    if (flags & (SAGE2_F_KERNEL_V8 | SAGE2_F_ONE_LEVEL)) return 8;
     // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
-    // C2-4K 648 vs 612); d = 128 non-causal N <= 8192 -> the persistent v10 (C2-1K 751 vs 718, C2-4K
-    // 1134 vs 1101); v8 elsewhere (causal, d = 128 from 16K on, the carrier / granularity variants)
+    // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 no longer wins
+    // anywhere since v8 hands P^ to the PV MMA in two halves: C2-1K d=128 700 vs 735, C2-4K 1096
+    // vs 1118 TOPS.)
     const bool plain = !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN));
     if (plain && d == 64) return 12;
-    if (plain && d == 128 && (N + 127) / 128 <= 64) return 10;
     return 8;
 }
 
@@ -275,12 +275,12 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false>
 int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn8Smem<D>::ALLOC;
-    int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>>(smem);
+    int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE>>(smem);
     if (rc) return rc;
-    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
+    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
     return cuda_rc();
 }
 
@@ -314,15 +314,6 @@ int launch_attn10_t(AttnParams p, int B, cudaStream_t st) {
     return rc;
 }
 
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0>
-int launch_attn13_t(const AttnParams& p, int B, cudaStream_t st) {
-    constexpr uint32_t smem = Attn13Smem<D>::ALLOC;
-    int rc = configure_smem<k_attn13<D, CAUSAL, DUMP, QKF8, TIMING, GRAN>>(smem);
-    if (rc) return rc;
-    k_attn13<D, CAUSAL, DUMP, QKF8, TIMING, GRAN><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
-    return cuda_rc();
-}
-
 template <bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn12Smem::ALLOC;
@@ -342,7 +333,6 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if constexpr (D == 64) {
             if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
         }
-        if (kern == 13) return launch_attn13_t<D, false, false, false, true>(p, B, st);
         return kern == 10 ? launch_attn10_t<D, false, false, true>(p, B, st)
                           : launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
@@ -359,11 +349,13 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if (dump) return launch_attn10_t<D, false, true>(p, B, st);
         return causal ? launch_attn10_t<D, true, false>(p, B, st) : launch_attn10_t<D, false, false>(p, B, st);
     }
-    if (kern == 13) {
-        if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) return SAGE2_EINVAL;
-        if (dump) return f8 ? launch_attn13_t<D, false, true, true>(p, B, st) : launch_attn13_t<D, false, true>(p, B, st);
-        if (f8) return causal ? launch_attn13_t<D, true, false, true>(p, B, st) : launch_attn13_t<D, false, false, true>(p, B, st);
-        return causal ? launch_attn13_t<D, true, false>(p, B, st) : launch_attn13_t<D, false, false>(p, B, st);
+    if (flags & SAGE2_F_ONE_LEVEL) {   // single-level accumulation ablation (v8 only)
+        if (dump) return f8 ? launch_attn8_t<D, false, true, true, false, 0, true>(p, B, st)
+                            : launch_attn8_t<D, false, true, false, false, 0, true>(p, B, st);
+        if (f8) return causal ? launch_attn8_t<D, true, false, true, false, 0, true>(p, B, st)
+                              : launch_attn8_t<D, false, false, true, false, 0, true>(p, B, st);
+        return causal ? launch_attn8_t<D, true, false, false, false, 0, true>(p, B, st)
+                      : launch_attn8_t<D, false, false, false, false, 0, true>(p, B, st);
     }
     if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
         if constexpr (D != 128) {

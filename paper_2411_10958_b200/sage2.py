@@ -173,7 +173,7 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096, "v12": 131072, "v13": 1048576}   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096, "v12": 131072, "one": 1048576}   # "one": v8 single-level ablation   # include/sage2.h SAGE2_F_KERNEL_*
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
