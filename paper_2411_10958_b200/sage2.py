@@ -135,24 +135,25 @@ def alloc_workspace(B, Hq, Hkv, N, d, device="cuda", causal=False):
 
 
 def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=False, smooth_v=False,
-         gran="thread"):
+         gran="thread", kernel="default"):
     """SageAttn2 forward: q [B,Hq,N,d], k/v [B,Hkv,N,d] fp16 CUDA -> out [B,Hq,N,d] fp16.
     qk_e4m3=True runs QK^T through the E4M3 carrier (kind::f8f6f4) instead of kind::i8;
     smooth_v=True subtracts V's column mean before the FP8 quantization and adds it back (P:304-306);
-    gran="block"/"token" selects the granularity-ablation quantization groups (d = 128 only)."""
+    gran="block"/"token" selects the granularity-ablation quantization groups (d = 128 only);
+    kernel forces an attention kernel / the single-level ablation ("v8", "v10", "v12", "one")."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     if out is None:
         out = torch.empty_like(q)
-    if workspace is None and not int8 and not qk_e4m3 and not smooth_v and gran == "thread":
+    if workspace is None and not int8 and not qk_e4m3 and not smooth_v and gran == "thread" and kernel == "default":
         _check(lib().sage2_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
                                 int(causal), _stream()))
         return out
     if workspace is None:
         workspace = alloc_workspace(B, Hq, Hkv, N, d, q.device)
     _check(lib().sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
-                               flags(causal, int8, qk_e4m3, smooth_v, gran), workspace.data_ptr(), workspace.numel(),
-                               _stream()))
+                               flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel], workspace.data_ptr(),
+                               workspace.numel(), _stream()))
     return out
 
 

@@ -653,3 +653,23 @@ def test_one_level_ablation(B, Hq, Hkv, N, d, causal, kind):
                                    OracleConfig(causal=causal, two_level=False), debug=True)
     err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
     print(f"one-level: max|err|={err:.3e} min cos={cos:.8f} rows beyond the bar={used}/{rows}")
+
+
+# accuracy floors against fp64 softmax attention (P:895 metrics), from profiles/r02_accuracy.json
+# (scripts/accuracy.py): lowest measured CosSim / highest Rel-L1 over all configs, with margin
+ACC_FLOORS = {"iid": (0.975, 0.23), "structured": (0.9995, 0.035)}
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(1, 1, 1, 256, 64, False), (2, 8, 8, 1024, 128, False),
+                                                 (1, 8, 2, 1500, 128, True), (1, 6, 6, 2000, 64, False)])
+@pytest.mark.parametrize("kind", ["iid", "structured"])
+def test_accuracy_vs_fp64_attention(B, Hq, Hkv, N, d, causal, kind):
+    """CosSim / Rel-L1 of the default path against softmax attention in fp64 (accuracy.py reference,
+    pinned to the oracle's exact mode) stay within the per-input-kind floors measured over C1-C4."""
+    from paper_2411_10958_b200 import accuracy
+    q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, kind=kind, seed=11, device="cuda")
+    out = sage2.attn(q, k, v, causal=causal)
+    torch.cuda.synchronize()
+    m = accuracy.evaluate(out, q, k, v, causal, [(b, h) for b in range(B) for h in range(Hq)], torch.arange(N))
+    cos_min, rl1_max = ACC_FLOORS[kind]
+    assert m["cos_sim"] >= cos_min and m["rel_l1"] <= rl1_max, m
