@@ -25,6 +25,7 @@ struct AttnParams {
     int32_t* s_dump;        // debug: [B*Hq][N_pad][N_pad] raw S_int (DUMP builds only)
     uint8_t* p_dump;        // debug: [B*Hq][N_pad][N_pad] P^ codes (DUMP builds only; may be null)
     int Hq, Hkv, N, nT;
+    int lpt;                // causal v8: CTAs in longest-first order over ALL heads (short sequences)
     float qk_scale_log2;    // log2(e)/sqrt(d)
 };
 

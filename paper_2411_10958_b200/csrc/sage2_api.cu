@@ -8,6 +8,7 @@
 //                    (clock64 phase-trace kernel builds, the FP22 accumulator probe, tensor-core and
 //                    unit microbenchmarks).  Never loaded by the product path.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <atomic>
@@ -394,6 +395,9 @@ int launch_attention(void* out, int32_t* s_dump, uint8_t* p_dump, int B, int Hq,
     p.Hkv = Hkv;
     p.N = N;
     p.nT = (N + 127) / 128;
+    // causal CTAs longest-first over all heads up to N = 8K (C2-1K d=128 459 -> 504, 4K 890 -> 939, 8K
+    // 1040 -> 1068 TOPS); head-major beyond (16K-100K d=128 lose 3-8% to L2 misses otherwise)
+    p.lpt = p.nT <= 64;
     p.qk_scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
     const bool dump = s_dump != nullptr && !(flags & SAGE2_F_DEBUG_TIMING);
     return d == 64 ? launch_attention_d<64>(p, B, flags, dump, st) : launch_attention_d<128>(p, B, flags, dump, st);
