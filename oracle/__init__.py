@@ -24,6 +24,7 @@ from .oracle import (  # noqa: F401
     ngroups,
     kv_head,
     q_block,
+    q_head_delta,
     delta_s,
     s_int_block,
     attn_block,

@@ -3,6 +3,7 @@
 No arithmetic of the method lives here: every number the oracle produces is computed in C.
 """
 import ctypes
+import dataclasses
 import os
 import subprocess
 import threading
@@ -32,7 +33,8 @@ def build(force=False):
 class _Cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in (
         "b_q", "kv_tile", "causal", "quant", "qk_max", "smooth_q", "smooth_k",
-        "pv_mode", "two_level", "smooth_v", "p_fp32", "qk_gran")] + [("amb_eta", ctypes.c_double)]
+        "pv_mode", "two_level", "smooth_v", "p_fp32", "qk_gran")] + [("amb_eta", ctypes.c_double),
+                                                                       ("q_delta", ctypes.c_float)]
 
 
 @dataclass
@@ -49,13 +51,15 @@ class OracleConfig:
     two_level: bool = True
     smooth_v: bool = False
     p_fp32: bool = False      # True: P^ decision in fp32 (diagnostic of C-21); default fp64 (paper verbatim)
-    qk_gran: int = 0          # 0 per-thread (SageAttn2), 1 per-block, 2 per-token (NEXT#4 ablation)
+    qk_gran: int = 0          # 0 per-thread (SageAttn2), 1 per-block, 2 per-token, 3 per-tensor (NEXT#4)
     amb_eta: float = 2.0 ** -21    # floor of the per-element ambiguity window (ex2.approx, C-21)
+    q_delta: float = 0.0      # qk_gran == 3: the head's delta_Q (set by sage2_forward_blocks / q_head_delta)
 
     def c(self):
         return _Cfg(self.b_q, self.kv_tile, int(self.causal), int(self.quant), self.qk_max,
                     int(self.smooth_q), int(self.smooth_k), self.pv_mode, int(self.two_level),
-                    int(self.smooth_v), int(self.p_fp32), int(self.qk_gran), float(self.amb_eta))
+                    int(self.smooth_v), int(self.p_fp32), int(self.qk_gran), float(self.amb_eta),
+                    float(self.q_delta))
 
 
 def lib():
@@ -84,6 +88,8 @@ def lib():
                 getattr(L, n).restype = None
             L.orc_kv_head.argtypes = [P, P, I, I, ctypes.POINTER(_Cfg), P, P, P, P, P, P, P]
             L.orc_q_block.argtypes = [P, I, I, ctypes.POINTER(_Cfg), P, P, P]
+            L.orc_q_head_delta.argtypes = [P, I, I, ctypes.POINTER(_Cfg)]
+            L.orc_q_head_delta.restype = ctypes.c_float
             L.orc_delta_s.argtypes = [P, P, I, I, P]
             L.orc_delta_s2.argtypes = [P, P, I, I, P, P]
             L.orc_s_int_block.argtypes = [P, P, I, I, P]
@@ -202,6 +208,14 @@ def q_block(Qblk, cfg=OracleConfig()):
     return r
 
 
+def q_head_delta(Q, cfg=OracleConfig()):
+    """Per-tensor granularity (qk_gran = 3): the head's delta_Q = max |gamma(Q_i)| over every block / qmax."""
+    Qb = _bits(Q)
+    N, d = Qb.shape
+    c = cfg.c()
+    return float(lib().orc_q_head_delta(_p(Qb), N, d, ctypes.byref(c)))
+
+
 def delta_s(qbar, kprime, with_abs=False):
     """Delta S_i = q_bar_i gamma(K)^T (O-7), fp64.  with_abs=True also returns sum_c |q_bar_c||K'_tc|."""
     qbar = _c(qbar, np.float32)
@@ -273,7 +287,7 @@ def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False, debug=F
     B, Hq, N, d = q.shape
     Hkv = k.shape[1]
     grp = Hq // Hkv
-    kv_cache = {}
+    kv_cache, qdelta = {}, {}
     outO, outO16, inter, flips = [], [], [], []
     for (b, h, i) in units:
         hk = h // grp
@@ -281,7 +295,12 @@ def sage2_forward_blocks(q, k, v, units, cfg=OracleConfig(), keep=False, debug=F
             kv_cache[(b, hk)] = kv_head(k[b, hk], v[b, hk], cfg)
         kv = kv_cache[(b, hk)]
         r0, r1 = 128 * i, min(128 * i + 128, N)
-        qb = q_block(q[b, h, r0:r1], cfg)
+        if cfg.qk_gran == 3:                         # per-tensor: the head's delta_Q first
+            if (b, h) not in qdelta:
+                qdelta[(b, h)] = q_head_delta(q[b, h], cfg)
+            qb = q_block(q[b, h, r0:r1], dataclasses.replace(cfg, q_delta=qdelta[(b, h)]))
+        else:
+            qb = q_block(q[b, h, r0:r1], cfg)
         if debug:
             ds, dsa = delta_s(qb["qbar"], kv["kprime"], with_abs=True)
             O, l, dbg = attn_block(qb, ds, kv, N, i, cfg, debug=True, ds_abs=dsa)

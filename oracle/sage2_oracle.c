@@ -63,11 +63,14 @@ typedef struct {
                        used to measure how many codes an fp32 implementation can flip (C-21)     */
     int qk_gran;    /* Q/K quantization granularity (NEXT#4 ablation):
                        0 per-thread (SageAttn2), 1 per-block (Q: 128-token block, K: 64-token
-                       block), 2 per-token (every token its own group)                   */
+                       block), 2 per-token (every token its own group), 3 per-tensor (one
+                       scale per head: max |gamma(Q)| over every block of the head / max |K'| over
+                       every key, the per-tensor quantizer of P:99 / row "Per-tensor" of P:1099)  */
     double amb_eta; /* additive floor of the per-element ambiguity window (relative distance of
                        448 P~ to an E4M3 rounding midpoint under which an fp32 implementation may
                        round the other way, C-21); the window itself is the fp32 error
                        bound of the score derived element by element in orc_attn_block_dbg     */
+    float q_delta;  /* qk_gran == 3: the head's per-tensor delta_Q (orc_q_head_delta); unused else */
 } orc_cfg;
 
 /* ------------------------------------------------------------------------------------------ */
@@ -168,10 +171,11 @@ int orc_group_k(int t) { return 4 * (t / 64) + (t % 8) / 2; }
 /* Granularity-general group maps (NEXT#4).  Q: token t of a 128-token block -> group in the block;
  * K: key token t -> group in the head.  Per-block groups follow SageAttention's blocks (b_q = 128,
  * b_k = 64); per-token groups are single tokens. */
-int orc_ngroups_q(int gran) { return gran == 1 ? 1 : gran == 2 ? 128 : 32; }
-int orc_ngroups_k128(int gran) { return gran == 1 ? 2 : gran == 2 ? 128 : 8; }   /* per 128 keys */
-int orc_group_q_g(int t, int gran) { return gran == 1 ? 0 : gran == 2 ? t : orc_group_q(t); }
-int orc_group_k_g(int t, int gran) { return gran == 1 ? t / 64 : gran == 2 ? t : orc_group_k(t); }
+int orc_ngroups_q(int gran) { return gran == 1 || gran == 3 ? 1 : gran == 2 ? 128 : 32; }
+/* per 128 keys; per-tensor (3): one group for the whole head, stored as group 0 */
+int orc_ngroups_k128(int gran) { return gran == 1 ? 2 : gran == 2 ? 128 : gran == 3 ? 1 : 8; }
+int orc_group_q_g(int t, int gran) { return gran == 1 || gran == 3 ? 0 : gran == 2 ? t : orc_group_q(t); }
+int orc_group_k_g(int t, int gran) { return gran == 1 ? t / 64 : gran == 2 ? t : gran == 3 ? 0 : orc_group_k(t); }
 
 /* ------------------------------------------------------------------------------------------ */
 /* Quantizer psi: delta = max|A|/qmax, A_hat = round(A/delta), clamp.              */
@@ -289,6 +293,7 @@ int orc_q_block(const uint16_t* Qblk, int n, int d, const orc_cfg* cfg,
             if (a > amax[g]) amax[g] = a;
         }
     for (int g = 0; g < ngq; ++g) dq[g] = f32_div(amax[g], (float)cfg->qk_max);
+    if (cfg->qk_gran == 3) dq[0] = cfg->q_delta;        /* per-tensor: the head's delta */
     memset(qhat, 0, (size_t)128 * d);
     for (int t = 0; t < n; ++t) {
         float delta = dq[orc_group_q_g(t, cfg->qk_gran)];
@@ -297,6 +302,24 @@ int orc_q_block(const uint16_t* Qblk, int n, int d, const orc_cfg* cfg,
     }
     free(qp);
     return 0;
+}
+
+/* Per-tensor granularity (qk_gran == 3, NEXT#4, "per-tensor"): delta_Q of a whole
+ * head = max over every Q block i and every element of |gamma(Q_i)| = |fp32(Q) - q_bar_i| (O-5),
+ * divided by qmax (O-6).  Q: [N, d] fp16 bits. */
+float orc_q_head_delta(const uint16_t* Q, int N, int d, const orc_cfg* cfg) {
+    float amax = 0.0f;
+    for (int r0 = 0; r0 < N; r0 += cfg->b_q) {
+        const int n = (N - r0 < cfg->b_q) ? N - r0 : cfg->b_q;
+        for (int c = 0; c < d; ++c) {
+            const float qb = cfg->smooth_q ? exact_mean_f32(Q + (size_t)r0 * d, d, 0, n, c) : 0.0f;
+            for (int t = 0; t < n; ++t) {
+                const float a = fabsf(f32_sub((float)orc_fp16_decode(Q[(size_t)(r0 + t) * d + c]), qb));
+                if (a > amax) amax = a;
+            }
+        }
+    }
+    return f32_div(amax, (float)cfg->qk_max);
 }
 
 /* O-7: Delta S_i[t] = q_bar_i . gamma(K)[t]   ("Delta S_ij = q_bar_i gamma(K_j)^T"),

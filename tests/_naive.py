@@ -55,7 +55,10 @@ def _qgroups_g(n_tokens, gran):
 
 
 def _kgroups_g(n_tokens, n_pad, gran):
-    """K groups for a granularity: 0 per-thread, 1 64-token blocks, 2 tokens."""
+    """K groups for a granularity: 0 per-thread, 1 64-token blocks, 2 tokens,
+    3 the whole head (per-tensor)."""
+    if gran == 3:
+        return [list(range(n_tokens))]
     if gran == 1:
         return [[t for t in range(b, b + 64) if t < n_tokens] for b in range(0, n_pad, 64)]
     if gran == 2:
@@ -104,14 +107,28 @@ def sage2_naive(Q, K, V, causal=False, kv_tile=128, qmax=7, p_fp32=False, gran=0
         for c in range(d):
             vhat[t, c] = 0.0 if dv[c] == 0 else _e4m3(np.float32(Vf[t, c] / dv[c]))
     O = np.zeros((N, d))
+    qdelta_tensor = None
+    if gran == 3:       # per-tensor: one delta_Q over every block's gamma(Q_i) of the head
+        amax = np.float32(0)
+        for b0 in range(0, N, 128):
+            Qb = Q[b0:b0 + 128]
+            qbar = np.array([_mean_f32(Qb[:, c].astype(np.float64)) for c in range(d)], np.float32)
+            amax = max(amax, np.float32(np.max(np.abs((Qb.astype(np.float32) - qbar).astype(np.float32)))))
+        qdelta_tensor = np.float32(amax / np.float32(qmax))
     for b0 in range(0, N, 128):
         rows = list(range(b0, min(b0 + 128, N)))
         Qb = Q[rows]
         qbar = np.array([_mean_f32(Qb[:, c].astype(np.float64)) for c in range(d)], np.float32)
         Qp = (Qb.astype(np.float32) - qbar).astype(np.float32)
-        qhat, dqs = _quant_groups(Qp, _qgroups_g(len(rows), gran), qmax, len(rows))
+        if gran == 3:
+            qhat = np.zeros((len(rows), d), np.int64)
+            if qdelta_tensor != 0:
+                qhat = np.clip(np.rint((Qp / qdelta_tensor).astype(np.float32)), -qmax, qmax).astype(np.int64)
+            dqs = [qdelta_tensor]
+        else:
+            qhat, dqs = _quant_groups(Qp, _qgroups_g(len(rows), gran), qmax, len(rows))
         dq_of = {}
-        for gi, toks in enumerate(_qgroups_g(len(rows), gran)):
+        for gi, toks in enumerate(_qgroups_g(len(rows), 1 if gran == 3 else gran)):
             for t in toks:
                 dq_of[t] = dqs[gi]
         dS = [sum(float(qbar[c]) * float(Kp[t, c]) for c in range(d)) for t in range(N)]

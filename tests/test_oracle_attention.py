@@ -215,16 +215,34 @@ def test_smooth_v_helps_channel_biased_v(orc):
     assert err[True] < err[False]
 
 
-@pytest.mark.parametrize("gran", [1, 2])
+@pytest.mark.parametrize("gran", [1, 2, 3])
 @pytest.mark.parametrize("N,kv_tile,causal", [(16, 4, True), (13, 128, False)])
 def test_granularity_vs_naive(orc, gran, N, kv_tile, causal):
-    """NEXT#4 ablation granularities (1 per-block, 2 per-token) against the naive implementation,
-    whose group lists are written out independently (tests/_naive.py)."""
+    """NEXT#4 ablation granularities (1 per-block, 2 per-token, 3 per-tensor) against the naive
+    implementation, whose group lists are written out independently (tests/_naive.py)."""
     d = 64
     Q, K, V = rnd((N, d), 29, 1, 2), rnd((N, d), 30, 1, -1), rnd((N, d), 31)
     ref = sage2_naive(Q, K, V, causal=causal, kv_tile=kv_tile, gran=gran)
     got = _oracle_head(orc, Q, K, V, OracleConfig(kv_tile=kv_tile, causal=causal, qk_gran=gran))
     assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_per_tensor_spans_blocks(orc):
+    """Per-tensor granularity takes ONE delta_Q over every Q block of the head (each
+    block smoothed by its own mean): a head of three blocks against the naive implementation, and
+    the delta equals the largest of the three per-block deltas."""
+    N, d = 300, 64
+    Q, K, V = rnd((N, d), 41, 1, 2), rnd((N, d), 42, 1, -1), rnd((N, d), 43)
+    Q[140:150] *= 6.0                    # the block with the outliers sets the head's scale
+    ref = sage2_naive(Q, K, V, kv_tile=128, gran=3)
+    got = _oracle_head(orc, Q, K, V, OracleConfig(qk_gran=3))
+    assert np.max(np.abs(got - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    dt = orc.q_head_delta(Q, OracleConfig(qk_gran=3))
+    per_block = [orc.q_block(Q[r:r + 128], OracleConfig(qk_gran=1))["dq"][0] for r in (0, 128, 256)]
+    assert dt == max(per_block)
+    kv = orc.kv_head(K, V, OracleConfig(qk_gran=3))
+    kv1 = orc.kv_head(K, V, OracleConfig(qk_gran=1))
+    assert kv["dk"][0] == max(kv1["dk"]) and not np.any(kv["dk"][1:])
 
 
 def test_granularity_accuracy_ordering(orc):
