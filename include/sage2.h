@@ -76,6 +76,8 @@ extern "C" {
                                   /* block, K: 64-token blocks) instead of per-thread      */
 #define SAGE2_F_GRAN_TOKEN 524288 /* NEXT#4 ablation: per-token Q/K quantization groups.  GRAN flags:     */
                                   /* d = 128, kernel v8 only.                                             */
+#define SAGE2_F_GRAN_TENSOR 2097152 /* NEXT#4 ablation: per-tensor Q/K scales (one per head,       */
+                                  /* P:1099); not with SMOOTH_V                                          */
 
 /* cudaGetErrorString of the last CUDA error an entry point of this thread returned SAGE2_ECUDA for. */
 const char* sage2_last_cuda_error(void);

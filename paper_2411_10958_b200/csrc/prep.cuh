@@ -23,11 +23,13 @@ namespace sage2 {
 constexpr int kTile = 128;  // b_q = b_kv = 128 tokens
 
 // Quantization granularity of Q and K (NEXT#4 ablation, oracle qk_gran): 0 per-thread (P:223,
-// SageAttn2), 1 per-block (Q: the 128-token block, K: 64-token blocks), 2 per-token.
-// Groups per 128 tokens (stored layout): Q 32 / 1 / 128, K 8 / 4 (2 used, padded for 16-byte bulk
-// copies) / 128.
-__host__ __device__ constexpr int gran_nq(int gran) { return gran == 1 ? 1 : gran == 2 ? 128 : 32; }
-__host__ __device__ constexpr int gran_nk(int gran) { return gran == 1 ? 4 : gran == 2 ? 128 : 8; }
+// SageAttn2), 1 per-block (Q: the 128-token block, K: 64-token blocks), 2 per-token, 3
+// per-tensor (one scale per head; stored in the per-block layout with every entry equal, so
+// the attention kernel runs its per-block instantiation).  4 (internal): the head-absmax pass of
+// per-tensor preprocessing.  Groups per 128 tokens (stored layout): Q 32 / 1 / 128 / 1, K 8 / 4
+// (2 used, padded for 16-byte bulk copies) / 128 / 4.
+__host__ __device__ constexpr int gran_nq(int gran) { return gran == 1 || gran >= 3 ? 1 : gran == 2 ? 128 : 32; }
+__host__ __device__ constexpr int gran_nk(int gran) { return gran == 1 || gran >= 3 ? 4 : gran == 2 ? 128 : 8; }
 
 
 // FP16 bits -> exact integer value * 2^24 (every finite fp16 is a multiple of 2^-24).
@@ -292,7 +294,9 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
                                                      const unsigned int* __restrict__ vmax, int8_t* __restrict__ khat,
                                                      float* __restrict__ dk, uint8_t* __restrict__ vhat,
                                                      float* __restrict__ kbar_out, float* __restrict__ dv_out,
-                                                     const float* __restrict__ vmean) {
+                                                     const float* __restrict__ vmean, unsigned int* ktmax = nullptr) {
+    // ktmax (per-tensor granularity): GRAN 4 accumulates max|K'| of the head into ktmax[bh] and
+    // stops; GRAN 3 then quantizes with delta_K = ktmax[bh] / qk_max for every group.
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // passes
     constexpr int VS = D + 8;                                       // padded V row (halves)
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
@@ -350,10 +354,22 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     }
     __syncthreads();
     constexpr int NGK = gran_nk(GRAN);
+    if constexpr (GRAN == 4) {
+        if (threadIdx.x < 32) {
+            float m = fmaxf(fmaxf(rowmax[threadIdx.x], rowmax[threadIdx.x + 32]),
+                            fmaxf(rowmax[threadIdx.x + 64], rowmax[threadIdx.x + 96]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (threadIdx.x == 0) atomicMax(ktmax + bh, __float_as_uint(m));   // |K'| >= 0: orders as uint
+        }
+        return;
+    }
     if (threadIdx.x < NGK) {
         const int g = threadIdx.x;
         float amax = 0.f;
-        if (GRAN == 2) {
+        if (GRAN == 3) {
+            amax = __uint_as_float(__ldcg(ktmax + bh));
+        } else if (GRAN == 2) {
             amax = rowmax[g];
         } else if (GRAN == 1) {
             if (g < 2)
@@ -372,7 +388,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 ? r / 64 : 4 * (r / 64) + (r % 8) / 2];
+        const float delta = gdelta[GRAN == 3 ? 0 : GRAN == 2 ? r : GRAN == 1 ? r / 64 : 4 * (r / 64) + (r % 8) / 2];
         int code[8];
         quant_codes8(kx[p], delta, __frcp_rn(delta), qk_max, code);
         *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = pack8_codes(code, e4m3_codes != 0);
@@ -426,7 +442,11 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
 template <int D, int GRAN = 0>
 __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q, int N, int qk_max, int e4m3_codes, int smooth_q,
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
-                                                    float* __restrict__ qbar_out, uint8_t* __restrict__ qbt) {
+                                                    float* __restrict__ qbar_out, uint8_t* __restrict__ qbt,
+                                                    unsigned int* qtmax = nullptr) {
+    // qtmax (per-tensor granularity): GRAN 4 accumulates max|gamma(Q_i)| of the head into qtmax[bh]
+    // and stops (q_bar and its images are written as usual); GRAN 3 quantizes with
+    // delta_Q = qtmax[bh] / qk_max.
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // d=128: 16 / 16 / 8; d=64: 8 / 32 / 4
     const int tile = blockIdx.x, bh = blockIdx.y, nT = gridDim.x;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -511,10 +531,22 @@ __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q
     }
     __syncthreads();
     constexpr int NGQ = gran_nq(GRAN);
+    if constexpr (GRAN == 4) {
+        if (threadIdx.x < 32) {
+            float m = fmaxf(fmaxf(rowmax[threadIdx.x], rowmax[threadIdx.x + 32]),
+                            fmaxf(rowmax[threadIdx.x + 64], rowmax[threadIdx.x + 96]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (threadIdx.x == 0) atomicMax(qtmax + bh, __float_as_uint(m));
+        }
+        return;
+    }
     if (threadIdx.x < NGQ) {
         const int g = threadIdx.x;
         float amax;
-        if (GRAN == 2) {
+        if (GRAN == 3) {
+            amax = __uint_as_float(__ldcg(qtmax + bh));
+        } else if (GRAN == 2) {
             amax = rowmax[g];
         } else if (GRAN == 1) {
             amax = 0.f;
@@ -532,7 +564,7 @@ __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int r = p * RPP + rofs;
-        const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 ? 0 : 8 * (r / 32) + (r % 8)];
+        const float delta = gdelta[GRAN == 2 ? r : GRAN == 1 || GRAN == 3 ? 0 : 8 * (r / 32) + (r % 8)];
         float x[8];
         gamma8(p, x);
         int code[8];

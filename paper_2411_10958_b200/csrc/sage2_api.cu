@@ -178,8 +178,9 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
 }
 
 constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12;
+constexpr int kGranFlags = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | SAGE2_F_GRAN_TENSOR;
 constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V | SAGE2_F_ONE_LEVEL |
-                            SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | kKernelFlags
+                            kGranFlags | kKernelFlags
 #ifdef SAGE2_DEV
                             | SAGE2_F_DEBUG_TIMING
 #endif
@@ -190,10 +191,11 @@ bool flags_ok(int flags) {
     const int kf = flags & kKernelFlags;
     if (kf & (kf - 1)) return false;                       // at most one kernel selector
     // granularity ablation: v8 only; v12: kind::i8 codes only
-    if ((flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) && (flags & SAGE2_F_KERNEL_V12)) return false;
+    if ((flags & kGranFlags) && (flags & SAGE2_F_KERNEL_V12)) return false;
     if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_KERNEL_V12)) return false;
-    const int granf = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN;
-    if ((flags & granf) == granf) return false;
+    const int granf = kGranFlags;
+    if ((flags & granf) & ((flags & granf) - 1)) return false;     // at most one granularity
+    if ((flags & SAGE2_F_GRAN_TENSOR) && (flags & SAGE2_F_SMOOTH_V)) return false;   // shares vsum
     // single-level ablation: v8 only, per-thread granularity
     if ((flags & SAGE2_F_ONE_LEVEL) && (flags & (granf | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12))) return false;
     // granularity ablation (NEXT#4): v8 at d = 128 only, no carrier
@@ -213,7 +215,7 @@ int kernel_of(int N, int d, int flags) {
     // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 no longer wins
     // anywhere since v8 hands P^ to the PV MMA in two halves: C2-1K d=128 700 vs 735, C2-4K 1096
     // vs 1118 TOPS.)
-    const bool plain = !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN));
+    const bool plain = !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | kGranFlags));
     if (plain && d == 64) return 12;
     return 8;
 }
@@ -244,17 +246,30 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     } else {
         k_kv_stats<D, false><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
     }
-    const int gran = (flags & SAGE2_F_GRAN_TOKEN) ? 2 : (flags & SAGE2_F_GRAN_BLOCK) ? 1 : 0;
-    auto kvq = gran == 2 ? k_kv_quant<D, 2> : gran == 1 ? k_kv_quant<D, 1> : k_kv_quant<D, 0>;
-    auto qq = gran == 2 ? k_q_quant<D, 2> : gran == 1 ? k_q_quant<D, 1> : k_q_quant<D, 0>;
-    kvq<<<dim3(nT, BHk), 256, 0, st>>>(
-        k, v, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, ksum, vmax, reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]),
-        reinterpret_cast<float*>(ws + L.off[R_DK]), ws + L.off[R_VHAT], reinterpret_cast<float*>(ws + L.off[R_KBAR]),
-        reinterpret_cast<float*>(ws + L.off[R_DV]), smv ? vmean : nullptr);
-    qq<<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, (flags & SAGE2_F_QK_E4M3) ? 1 : 0, smooth_q,
-                                      reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]),
-                                      reinterpret_cast<float*>(ws + L.off[R_DQ]),
-                                      reinterpret_cast<float*>(ws + L.off[R_QBAR]), ws + L.off[R_QBT]);
+    const int gran = (flags & SAGE2_F_GRAN_TENSOR) ? 3 : (flags & SAGE2_F_GRAN_TOKEN) ? 2 : (flags & SAGE2_F_GRAN_BLOCK) ? 1 : 0;
+    auto kvq = gran == 3 ? k_kv_quant<D, 3> : gran == 2 ? k_kv_quant<D, 2> : gran == 1 ? k_kv_quant<D, 1> : k_kv_quant<D, 0>;
+    auto qq = gran == 3 ? k_q_quant<D, 3> : gran == 2 ? k_q_quant<D, 2> : gran == 1 ? k_q_quant<D, 1> : k_q_quant<D, 0>;
+    // per-tensor granularity: the heads' max |K'| / max |gamma(Q_i)| first (GRAN 4 passes, atomics
+    // into the zeroed vsum region, unused without smooth V)
+    auto* ktmax = reinterpret_cast<unsigned int*>(vsum);
+    auto* qtmax = ktmax + BHk;
+    const int e4 = (flags & SAGE2_F_QK_E4M3) ? 1 : 0;
+    auto* khat_p = reinterpret_cast<int8_t*>(ws + L.off[R_KHAT]);
+    auto* dk_p = reinterpret_cast<float*>(ws + L.off[R_DK]);
+    auto* kbar_p = reinterpret_cast<float*>(ws + L.off[R_KBAR]);
+    auto* dv_p = reinterpret_cast<float*>(ws + L.off[R_DV]);
+    auto* qhat_p = reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]);
+    auto* dq_p = reinterpret_cast<float*>(ws + L.off[R_DQ]);
+    auto* qbar_p = reinterpret_cast<float*>(ws + L.off[R_QBAR]);
+    if (gran == 3) {
+        k_kv_quant<D, 4><<<dim3(nT, BHk), 256, 0, st>>>(k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
+                                                        kbar_p, dv_p, nullptr, ktmax);
+        k_q_quant<D, 4><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT],
+                                                       qtmax);
+    }
+    kvq<<<dim3(nT, BHk), 256, 0, st>>>(k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p, dv_p,
+                                       smv ? vmean : nullptr, ktmax);
+    qq<<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
     // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
@@ -358,7 +373,7 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         return causal ? launch_attn8_t<D, true, false, false, false, 0, true>(p, B, st)
                       : launch_attn8_t<D, false, false, false, false, 0, true>(p, B, st);
     }
-    if (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)) {   // NEXT#4 granularity ablation (d = 128)
+    if (flags & kGranFlags) {   // NEXT#4 granularity ablation (d = 128); per-tensor runs the per-block kernel
         if constexpr (D != 128) {
             return SAGE2_EINVAL;
         } else {
@@ -478,7 +493,7 @@ int sage2_debug_qk_int32(void* out, int32_t* s_int, uint8_t* p_hat, int B, int H
     int rc = check_device();
     if (rc) return rc;
     if (!shapes_ok(B, H_q, H_kv, N, d) || !out || !s_int || !workspace || !aligned16(out) || !aligned256(workspace) ||
-        !flags_ok(flags) || (flags & (SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN)))
+        !flags_ok(flags) || (flags & kGranFlags))
         return SAGE2_EINVAL;
     Layout L = make_layout(B, H_q, H_kv, N, d);
     if (ws_bytes < L.off[R_END]) return SAGE2_EINVAL;

@@ -110,7 +110,7 @@ def _check_inputs(q, k, v):
 
 F_QK_E4M3 = 2048    # include/sage2.h SAGE2_F_QK_E4M3 (E4M3-carrier QK^T variant)
 F_SMOOTH_V = 32768  # include/sage2.h SAGE2_F_SMOOTH_V (optional smooth V)
-F_GRAN = {"thread": 0, "block": 262144, "token": 524288}   # SAGE2_F_GRAN_* (NEXT#4 ablation)
+F_GRAN = {"thread": 0, "block": 262144, "token": 524288, "tensor": 2097152}   # SAGE2_F_GRAN_* (NEXT#4 ablation)
 
 
 def flags(causal=False, int8=False, qk_e4m3=False, smooth_v=False, gran="thread"):

@@ -1,6 +1,7 @@
 """NEXT#4: QK quantization granularity ablation on B200 (the paper's P:1089-1106 speed table and
 P:540-547 accuracy table, re-measured): per-thread (SageAttn2 default) / per-block / per-token.
 
+  (per-tensor added in round 2: one scale per head)
   speed:    attention kernel TOPS at C2-32K d=128 (B=4, H=32, N=32768), non-causal and causal
   accuracy: CosSim / Rel-L1 / RMSE against fp32 attention (torch SDPA, TF32 off) on the
             'structured' synthetic inputs (channel outliers) at B=1, H=8, N=4096
@@ -20,7 +21,7 @@ res = {"speed": {}, "accuracy": {}}
 B, H, N, d = 4, 32, 32768, 128
 q, k, v = synth.make_qkv(B, H, H, N, d, device="cuda")
 ops = 4.0 * B * H * N * N * d
-for gran in ("thread", "block", "token"):
+for gran in ("thread", "block", "token", "tensor"):
     for causal in (False, True):
         ws = sage2.alloc_workspace(B, H, H, N, d)
         sage2.prepare(q, k, v, ws, causal=causal, gran=gran)
@@ -43,7 +44,7 @@ del q, k, v
 B, H, N = 1, 8, 4096
 q, k, v = synth.make_qkv(B, H, H, N, d, kind="structured", seed=3, device="cuda")
 ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
-for gran in ("thread", "block", "token"):
+for gran in ("thread", "block", "token", "tensor"):
     o = sage2.attn(q, k, v, gran=gran).float()
     cos = torch.nn.functional.cosine_similarity(o.flatten(), ref.flatten(), dim=0).item()
     rl1 = ((o - ref).abs().sum() / ref.abs().sum()).item()

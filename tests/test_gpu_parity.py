@@ -447,13 +447,14 @@ def test_causal_compact_delta_s(N, d):
     assert sage2.workspace_bytes(1, 32, 8, 100000, 128, causal=True) < 0.55 * sage2.workspace_bytes(1, 32, 8, 100000, 128)
 
 
-@pytest.mark.parametrize("gran", ["block", "token"])
+@pytest.mark.parametrize("gran", ["block", "token", "tensor"])
 @pytest.mark.parametrize("B,Hq,Hkv,N,causal", [(1, 2, 1, 300, False), (2, 4, 2, 384, True)])
 def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
-    """NEXT#4: per-block / per-token Q/K groups.  Codes and scales bit-exact against the oracle's
-    qk_gran, outputs within the same bar as the default (d = 128, kernel v8)."""
+    """NEXT#4: per-block / per-token / per-tensor Q/K scales.  Codes and scales bit-exact against the
+    oracle's qk_gran, outputs within the same bar as the default (d = 128, kernel v8).  Per-tensor is
+    stored in the per-block layout (every entry the head's scale)."""
     d = 128
-    gi = {"block": 1, "token": 2}[gran]
+    gi = {"block": 1, "token": 2, "tensor": 3}[gran]
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=21)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
     sage2.prepare(qg, kg, vg, ws, causal=causal, gran=gran)
@@ -464,7 +465,7 @@ def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
     g = read_prepared(ws, lay, B, Hq, Hkv, N, d)
     nT = (N + 127) // 128
     nq, nk = orc.ngroups(gi)
-    nk_store = 4 if gi == 1 else nk
+    nk_store = 4 if gi in (1, 3) else nk
     dq = region(ws, lay, "dq", np.float32, B * Hq * nT * nq).reshape(B * Hq, nT, nq)
     dk = region(ws, lay, "dk", np.float32, B * Hkv * nT * nk_store).reshape(B * Hkv, nT, nk_store)
     cfg = OracleConfig(causal=causal, qk_gran=gi)
@@ -472,10 +473,17 @@ def test_granularity_ablation_parity(gran, B, Hq, Hkv, N, causal):
         for hk in range(Hkv):
             kv = orc.kv_head(k.numpy()[b, hk], v.numpy()[b, hk], cfg)
             assert np.array_equal(g["khat"][b * Hkv + hk], kv["khat"])
-            assert np.array_equal(dk[b * Hkv + hk, :, :nk].reshape(-1).view(np.uint32), kv["dk"].view(np.uint32))
+            if gi == 3:     # per-tensor: every stored entry is the head's delta_K (oracle group 0)
+                assert np.all(dk[b * Hkv + hk].view(np.uint32) == kv["dk"][:1].view(np.uint32))
+            else:
+                assert np.array_equal(dk[b * Hkv + hk, :, :nk].reshape(-1).view(np.uint32), kv["dk"].view(np.uint32))
         for hq in range(Hq):
+            qcfg = cfg
+            if gi == 3:
+                import dataclasses
+                qcfg = dataclasses.replace(cfg, q_delta=orc.q_head_delta(q.numpy()[b, hq], cfg))
             for i in range(nT):
-                qb = orc.q_block(q.numpy()[b, hq, 128 * i:min(N, 128 * i + 128)], cfg)
+                qb = orc.q_block(q.numpy()[b, hq, 128 * i:min(N, 128 * i + 128)], qcfg)
                 assert np.array_equal(g["qhat"][b * Hq + hq, 128 * i:128 * i + 128], qb["qhat"])
                 assert np.array_equal(dq[b * Hq + hq, i].view(np.uint32), qb["dq"].view(np.uint32))
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)]
