@@ -59,7 +59,7 @@ extern "C" {
                                   /* tensor-core GEMM (the default for N <= 2048 anyway)                  */
 #define SAGE2_F_QK_E4M3 2048      /* E4M3-carrier QK^T: the INT4 codes stored as E4M3 bytes and S on      */
                                   /* kind::f8f6f4 (fp32 accumulator, the same integer S; C-24). */
-                                  /* Not with INT8 or KERNEL_V10.                                         */
+                                  /* Not with INT8, KERNEL_V10 or KERNEL_V12.                             */
 #define SAGE2_F_KERNEL_V8 4096    /* force the v8 attention kernel (csrc/attn8.cuh)                        */
 #define SAGE2_F_KERNEL_V10 16384  /* force the persistent v10 kernel (csrc/attn10.cuh; one CTA per SM      */
                                   /* looping over (Q-block pair, h_q, b) items).  Not with QK_E4M3/GRAN.  */
@@ -143,8 +143,8 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
 /* Which attention kernel sage2_attention runs for (N, d, flags): 12, 10 or 8 (SAGE2_F_KERNEL_V12 /
- * _V10 / _V8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64 non-causal, 10 for d = 128
- * non-causal N <= 8192; 8 otherwise).  Host-only, no CUDA call; never fails. */
+ * _V10 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
+ * non-causal, 8 otherwise).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
 /* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263), on a workspace filled by
