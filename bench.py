@@ -132,8 +132,14 @@ def dist_setup(n_gpus):
     if world > 1:
         import torch.distributed as dist
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # SAGE2_DIST_BACKEND=gloo (test hook): several ranks on fewer GPUs (rank -> device
+            # local % count) so the multi-rank path can be exercised on a one-GPU box; NCCL otherwise
+            backend = os.environ.get("SAGE2_DIST_BACKEND", "nccl")
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group(backend)
         else:                               # CPU dry runs of the launch path (tests: --dist-check)
             dist.init_process_group("gloo")
     elif torch.cuda.is_available():
@@ -254,7 +260,7 @@ def run_ours(args, world, rank, local):
     name = args.config
     B, Hq, Hkv, N, d, causal, kind = CONFIGS[name]
     grp = Hq // Hkv
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", (local % torch.cuda.device_count()) if world > 1 else 0)
     strong = args.scaling == "strong"
     if strong:
         # this rank's share of the config's fixed unit list, run as [n_units, grp, N, d] (H_kv = 1 per unit)
@@ -368,7 +374,8 @@ def run_ours(args, world, rank, local):
                                   causal=causal)[0]
             bad = shard.first_unit_check(parts, recompute)
         del parts
-        validation = {"collective": "all_gather (NCCL)", "gathered_bytes": int(out.numel() * 2 * world),
+        import torch.distributed as dist
+        validation = {"collective": f"all_gather ({dist.get_backend()})", "gathered_bytes": int(out.numel() * 2 * world),
                       "gather_ms_wall": g_ms, "ranks_mismatched": bad,
                       "check": "rank 0 recomputes every rank's first unit alone: bitwise equal"}
     kver = sage2.attention_kernel(N, d, causal=causal)
