@@ -93,7 +93,8 @@ const char* sage2_strerror(int code);
  * N_pad = ceil(N/128)*128).  Returns 0 for invalid shapes. */
 size_t sage2_workspace_bytes(int B, int H_q, int H_kv, int N, int d, int causal);
 
-/* Full forward pass (preprocessing + attention kernel) -- the north-star entry point.  Allocates its
+/* Full forward pass (preprocessing + attention kernel; Alg. 1, Fig. 3) -- the
+ * north-star entry point: out = SageAttn2-4b(q, k, v), softmax scale 1/sqrt(d).  Allocates its
  * workspace stream-ordered from the library's per-device pool (cudaMallocFromPoolAsync /
  * cudaFreeAsync on `stream`); the pool keeps the peak footprint mapped for the next call until
  * sage2_release_memory().  causal: 0 or 1.  Errors: SAGE2_EINVAL (shape, null / misaligned pointer),
@@ -110,7 +111,8 @@ int sage2_attn_ws(const void* q, const void* k, const void* v, void* out, int B,
 int sage2_attn_ex(const void* q, const void* k, const void* v, void* out, int B, int H_q, int H_kv, int N,
                   int d, int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* End-to-end call on HOST buffers (page-locked memory required for copy/compute overlap; same
+/* End-to-end call on HOST buffers (the same computation as sage2_attn, Alg. 1; page-locked
+ * memory required for copy/compute overlap; same
  * layouts as above).  Pipelined over up to 16 chunks of (b, h_kv) units on three internal streams:
  * each chunk's H2D copy, preprocessing, attention and D2H copy are stream-ordered, so one chunk's
  * copies overlap the others' kernels.  Device buffers (three chunk sets) are allocated and freed
@@ -138,7 +140,11 @@ int sage2_attn_host(const void* q_host, const void* k_host, const void* v_host, 
 #define SAGE2_WS_NREGIONS 15
 int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offsets);
 
-/* Preprocessing only (Fig. 3 steps 1-3): fills the workspace regions listed above. */
+/* Preprocessing only (Fig. 3 steps 1-3; Alg. 1 "Preprocessing" P:241 and the per-block Q line P:248):
+ * k_bar and gamma(K), q_bar_i and gamma(Q_i), Delta S_i = q_bar_i gamma(K)^T
+ * (P:193), per-thread INT4 groups of Q / K (INT8 with SAGE2_F_INT8), per-channel
+ * E4M3 V; fills the workspace regions listed above.  Errors: SAGE2_EINVAL (shape, flags,
+ * pointer / workspace size or alignment), SAGE2_EUNSUPPORTED, SAGE2_ECUDA. */
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
@@ -147,7 +153,9 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
  * non-causal, 8 otherwise).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
-/* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263), on a workspace filled by
+/* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263: S = psi^-1(Q^K^T) + Delta S,
+ * online softmax, P^ = e4m3(448 P~), R = P^V^ and O = alpha O + R,
+ * O / l / 448 * delta_V), on a workspace filled by
  * sage2_prepare with the same shapes and data flags (256-byte aligned, at least
  * sage2_workspace_bytes).  The workspace is only read: several sage2_attention calls may share one
  * prepared workspace, also concurrently on different streams.  The persistent v10 kernel takes its
