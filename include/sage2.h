@@ -59,11 +59,8 @@ extern "C" {
                                   /* tensor-core GEMM (the default for N <= 2048 anyway)                  */
 #define SAGE2_F_QK_E4M3 2048      /* E4M3-carrier QK^T: the INT4 codes stored as E4M3 bytes and S on      */
                                   /* kind::f8f6f4 (fp32 accumulator, the same integer S; C-24). */
-                                  /* Not with INT8, KERNEL_V10 or KERNEL_V12.                             */
+                                  /* Not with INT8 or KERNEL_V12.                                         */
 #define SAGE2_F_KERNEL_V8 4096    /* force the v8 attention kernel (csrc/attn8.cuh)                        */
-#define SAGE2_F_KERNEL_V10 16384  /* force the persistent v10 kernel (csrc/attn10.cuh; one CTA per SM      */
-                                  /* looping over (Q-block pair, h_q, b) items).  Not with QK_E4M3/GRAN.  */
-                                  /* No kernel flag: sage2_attention_kernel answers which kernel runs.    */
 #define SAGE2_F_KERNEL_V12 131072 /* force the v12 kernel (csrc/attn12.cuh, d = 64 only: four Q tiles per  */
                                   /* CTA, b_kv = 64 -- the oracle's kv_tile is then 64, reading C-9).      */
                                   /* Not with QK_E4M3 / GRAN flags.                                       */
@@ -148,8 +145,8 @@ int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offse
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* Which attention kernel sage2_attention runs for (N, d, flags): 12, 10 or 8 (SAGE2_F_KERNEL_V12 /
- * _V10 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
+/* Which attention kernel sage2_attention runs for (N, d, flags): 12 or 8 (SAGE2_F_KERNEL_V12 /
+ * _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
  * non-causal, 8 otherwise).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
@@ -158,13 +155,12 @@ int sage2_attention_kernel(int N, int d, int flags);
  * O / l / 448 * delta_V), on a workspace filled by
  * sage2_prepare with the same shapes and data flags (256-byte aligned, at least
  * sage2_workspace_bytes).  The workspace is only read: several sage2_attention calls may share one
- * prepared workspace, also concurrently on different streams.  The persistent v10 kernel takes its
- * work counters from a per-launch 256-byte block of the library pool. */
+ * prepared workspace, also concurrently on different streams.  */
 int sage2_attention(void* out, int B, int H_q, int H_kv, int N, int d, int flags, const void* workspace,
                     size_t ws_bytes, void* stream);
 
 /* Debug (parity tests): runs the attention kernel sage2_attention would run for (N, d, flags)
- * non-causally (a KERNEL flag selects v8 or v10) and additionally writes the raw INT32 QK^T
+ * non-causally (a KERNEL flag selects v8 or v12) and additionally writes the raw INT32 QK^T
  * accumulators read back from TMEM to s_int [B*H_q][N_pad][N_pad] (device, caller-owned,
  * 4*B*H_q*N_pad^2 bytes; intended for small N) and, if p_hat is not NULL, the E4M3 codes of
  * P^ = e4m3(448 P~) the kernel fed to the PV MMA, [B*H_q][N_pad][N_pad] bytes (the codes of KV tile j

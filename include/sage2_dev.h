@@ -17,7 +17,7 @@ extern "C" {
 #define SAGE2_F_DEBUG_TIMING 64 /* internal: clock64 phase-stamp builds of the attention kernels */
 
 /* clock64 phase trace of the attention kernel sage2_attention would run (non-causal; a KERNEL flag
- * selects v8 / v10): stamps of CTA (0,0,0) written to `stamps` (device, caller-owned, zeroed,
+ * selects v8 / v12): stamps of CTA (0,0,0) written to `stamps` (device, caller-owned, zeroed,
  * uint64 [32 roles][64 KV steps][16 slots]; the slot meaning is in the kernel source (ts / tss
  * calls)).  out receives the output. */
 int sage2_dev_trace(void* out, uint64_t* stamps, int B, int H_q, int H_kv, int N, int d, int flags,

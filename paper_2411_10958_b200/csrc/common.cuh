@@ -5,7 +5,7 @@
 #include <cstdint>
 
 #ifndef SAGE2_PSPLIT
-#define SAGE2_PSPLIT 1   // v8/v10: hand P^ to the PV MMA in two halves (A/B builds: 0 = one hand-off per tile)
+#define SAGE2_PSPLIT 1   // v8: hand P^ to the PV MMA in two halves (A/B builds: 0 = one hand-off per tile)
 #endif
 
 namespace sage2 {

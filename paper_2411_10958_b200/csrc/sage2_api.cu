@@ -1,6 +1,6 @@
 // sage2_api.cu -- the C ABI of libsage2.so (include/sage2.h): validation, workspace layout,
 // stream-ordered launches of the preprocessing kernels (prep.cuh, dsg.cuh) and the tcgen05
-// attention kernels (attn8.cuh, attn10.cuh).
+// attention kernels (attn8.cuh, attn12.cuh).
 //
 // Built twice from this one source (paper_2411_10958_b200/build.py):
 //   libsage2.so      the product: only the entry points of include/sage2.h;
@@ -19,7 +19,6 @@
 #include <vector>
 
 #include "../../include/sage2.h"
-#include "attn10.cuh"
 #include "attn12.cuh"
 #include "attn8.cuh"
 #include "dsg.cuh"
@@ -177,7 +176,7 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12;
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12;
 constexpr int kGranFlags = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | SAGE2_F_GRAN_TENSOR;
 constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V | SAGE2_F_ONE_LEVEL |
                             kGranFlags | kKernelFlags
@@ -197,11 +196,11 @@ bool flags_ok(int flags) {
     if ((flags & granf) & ((flags & granf) - 1)) return false;     // at most one granularity
     if ((flags & SAGE2_F_GRAN_TENSOR) && (flags & SAGE2_F_SMOOTH_V)) return false;   // shares vsum
     // single-level ablation: v8 only, per-thread granularity
-    if ((flags & SAGE2_F_ONE_LEVEL) && (flags & (granf | SAGE2_F_KERNEL_V10 | SAGE2_F_KERNEL_V12))) return false;
+    if ((flags & SAGE2_F_ONE_LEVEL) && (flags & (granf | SAGE2_F_KERNEL_V12))) return false;
     // granularity ablation (NEXT#4): v8 at d = 128 only, no carrier
-    if ((flags & granf) && (flags & (SAGE2_F_QK_E4M3 | SAGE2_F_KERNEL_V10))) return false;
+    if ((flags & granf) && (flags & SAGE2_F_QK_E4M3)) return false;
     // the E4M3 carrier holds the INT4 codes only (|c| <= 7); v8 and v11 only
-    if ((flags & SAGE2_F_QK_E4M3) && (flags & (SAGE2_F_INT8 | SAGE2_F_KERNEL_V10))) return false;
+    if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_INT8)) return false;
     return true;
 }
 
@@ -209,12 +208,11 @@ bool flags_ok(int flags) {
 // kernel fixes the order of the keys inside the V^T tile images and Delta S rows).
 int kernel_of(int N, int d, int flags) {
     if (flags & SAGE2_F_KERNEL_V12) return 12;
-    if (flags & SAGE2_F_KERNEL_V10) return 10;
     if (flags & (SAGE2_F_KERNEL_V8 | SAGE2_F_ONE_LEVEL)) return 8;
     // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
-    // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 no longer wins
-    // anywhere since v8 hands P^ to the PV MMA in two halves: C2-1K d=128 700 vs 735, C2-4K 1096
-    // vs 1118 TOPS.)
+    // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 of round 1 lost
+    // everywhere once v8 handed P^ to the PV MMA in two halves -- C2-1K d=128 706 vs 735, causal 438
+    // vs 502, C2-4K 1096 vs 1118 TOPS -- and was removed.)
     const bool plain = !(flags & (SAGE2_F_CAUSAL | SAGE2_F_QK_E4M3 | kGranFlags));
     if (plain && d == 64) return 12;
     return 8;
@@ -300,36 +298,6 @@ int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
-// The persistent kernel's work counters live in a per-launch buffer from the library pool, zeroed on
-// the launch stream right before the launch: concurrent launches (other streams, shared workspaces)
-// never share counters, and the workspace stays read-only for sage2_attention.
-template <int D, bool CAUSAL, bool DUMP, bool TIMING = false>
-int launch_attn10_t(AttnParams p, int B, cudaStream_t st) {
-    constexpr uint32_t smem = Attn10Smem<D>::ALLOC;
-    int rc = configure_smem<k_attn10<D, CAUSAL, DUMP, false, TIMING>>(smem);
-    if (rc) return rc;
-    int nsm = 0;
-    if ((rc = sm_count(&nsm))) return rc;
-    const long long nitems = (long long)((p.nT + 1) / 2) * p.Hq * B;
-    if (nitems > 0x7fffffff) return SAGE2_EINVAL;
-    const int grid = (int)(nitems < nsm ? nitems : nsm);   // persistent: one CTA per SM
-    void* ctr = nullptr;
-    if (lib_malloc_async(&ctr, 256, st) != cudaSuccess) {
-        cudaGetLastError();
-        return SAGE2_ENOMEM;
-    }
-    if (cudaMemsetAsync(ctr, 0, 8, st) != cudaSuccess) {
-        rc = cuda_rc();
-        cudaFreeAsync(ctr, st);
-        return rc;
-    }
-    p.sched = static_cast<unsigned int*>(ctr);
-    k_attn10<D, CAUSAL, DUMP, false, TIMING><<<grid, 640, smem, st>>>(p, (int)nitems);
-    rc = cuda_rc();
-    if (cudaFreeAsync(ctr, st) != cudaSuccess && rc == SAGE2_OK) rc = cuda_rc();
-    return rc;
-}
-
 template <bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn12Smem::ALLOC;
@@ -349,8 +317,7 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if constexpr (D == 64) {
             if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
         }
-        return kern == 10 ? launch_attn10_t<D, false, false, true>(p, B, st)
-                          : launch_attn8_t<D, false, false, false, true>(p, B, st);
+        return launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
 #endif
     if (kern == 12) {     // four Q tiles per CTA, b_kv = 64: head dim 64 only
@@ -360,10 +327,6 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
             if (dump) return launch_attn12_t<false, true>(p, B, st);
             return causal ? launch_attn12_t<true, false>(p, B, st) : launch_attn12_t<false, false>(p, B, st);
         }
-    }
-    if (kern == 10) {
-        if (dump) return launch_attn10_t<D, false, true>(p, B, st);
-        return causal ? launch_attn10_t<D, true, false>(p, B, st) : launch_attn10_t<D, false, false>(p, B, st);
     }
     if (flags & SAGE2_F_ONE_LEVEL) {   // single-level accumulation ablation (v8 only)
         if (dump) return f8 ? launch_attn8_t<D, false, true, true, false, 0, true>(p, B, st)

@@ -140,7 +140,7 @@ def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=Fa
     qk_e4m3=True runs QK^T through the E4M3 carrier (kind::f8f6f4) instead of kind::i8;
     smooth_v=True subtracts V's column mean before the FP8 quantization and adds it back (P:304-306);
     gran="block"/"token" selects the granularity-ablation quantization groups (d = 128 only);
-    kernel forces an attention kernel / the single-level ablation ("v8", "v10", "v12", "one")."""
+    kernel forces an attention kernel / the single-level ablation ("v8", "v12", "one")."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     if out is None:
@@ -174,13 +174,13 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v10": 16384, "v8": 4096, "v12": 131072, "one": 1048576}   # "one": v8 single-level ablation   # include/sage2.h SAGE2_F_KERNEL_*
+KERNEL_FLAGS = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576}   # include/sage2.h SAGE2_F_KERNEL_*; "one": v8 single-level ablation
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
               smooth_v=False, gran="thread"):
     """The tcgen05 attention kernel only, on a prepared workspace (kernel: "default" = the dispatch
-    rule of sage2_attention_kernel, or "v8" / "v10"; data flags must match the prepare() call)."""
+    rule of sage2_attention_kernel, or "v8" / "v12" / "one"; data flags must match the prepare() call)."""
     _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
                                  flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
@@ -194,7 +194,7 @@ def attention_kernel(N, d, causal=False, kernel="default", qk_e4m3=False, gran="
 
 def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False, kernel="default",
                    smooth_v=False):
-    """Runs the attention kernel (non-causal; kernel: "default" dispatch rule, "v8" or "v10") and
+    """Runs the attention kernel (non-causal; kernel: "default" dispatch rule, "v8" or "v12") and
     returns the raw INT32 S = Q^ K^T read from TMEM, [B*Hq, N_pad, N_pad] (and, with_p=True, also
     the P^ E4M3 codes the kernel produced)."""
     Np = (N + 127) // 128 * 128

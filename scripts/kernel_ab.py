@@ -2,7 +2,7 @@
 
     python scripts/kernel_ab.py N d [variants] [rounds] [B] [H]
 
-variants: comma list of NAME or NAME@LIB, where NAME is default / v8 / v10 (suffix _causal for the
+variants: comma list of NAME or NAME@LIB, where NAME is default / v8 / v12 / one (suffix _causal for the
 causal mask, _f8 for the E4M3 carrier) and LIB the path of an A/B build of the library
 (paper_2411_10958_b200.build.build(out=..., defines=...)); default: the in-tree libsage2.so.  Each
 library prepares its own workspace.  Variants are timed round-robin (5 launches each per round) so
@@ -23,7 +23,7 @@ names = (sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] else "default").split(
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 B = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 H = int(sys.argv[6]) if len(sys.argv) > 6 else 32
-KF = {"default": 0, "v8": 4096, "v10": 16384, "v12": 131072, "one": 1048576}
+KF = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576}
 q, k, v = synth.make_qkv(B, H, H, N, d, device="cuda")
 out = torch.empty_like(q)
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)

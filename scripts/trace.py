@@ -1,4 +1,4 @@
-"""Per-phase clock64 stamps of one CTA of the v8 (or v10: KERNEL=v10) attention kernel (dev library:
+"""Per-phase clock64 stamps of one CTA of the v8 (or KERNEL=v12) attention kernel (dev library:
 sage2.trace).  python scripts/trace.py [N] [d]
 Softmax tile k (thread 0 of its half-0 warpgroup), slots: 0 loop start, 1 S ready, 9 S loaded,
 2 dequant, 3 max exchanged, 4 MUFU turn, 5 P^ written, 6 R ready, 7 R read, 8 promotion done.

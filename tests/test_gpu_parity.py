@@ -3,7 +3,7 @@
 The oracle is the paper-verbatim one (OracleConfig defaults: fp64 scores, P~ = exp(S - m) in fp64
 and P^ = E4M3(448 P~) decided in fp64).  Bar:
   * codes, scales, means (Q^, K^, V^, delta_Q, delta_K, delta_V, q_bar, k_bar): bit-exact;
-  * S_int = Q^ K^T read back from TMEM: bit-exact (v8 and v10, up to N = 2048: 16 KV tiles, so
+  * S_int = Q^ K^T read back from TMEM: bit-exact (v8 and v12, up to N = 2048: 16 KV tiles, so
     the 3-stage K/V ring wraps around several times);
   * Delta S: |gpu - oracle| <= 2e-6 * sum_c |q_bar_c| |K'_tc|   (fp32 FMA chain vs fp64 sum);
   * P^ = e4m3(448 P~) codes the kernel fed to the PV MMA: identical to the oracle's except where
@@ -89,12 +89,11 @@ def test_preprocess_bit_exact(B, Hq, Hkv, N, d, kind, int8):
                     assert np.all(np.abs(got - ds) <= bound + 1e-6 * np.abs(ds))
 
 
-@pytest.mark.parametrize("kernel", ["v8", "v10"])
+@pytest.mark.parametrize("kernel", ["v8"])
 @pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128), (1024, 128), (2048, 64), (1900, 128)])
 def test_s_int_bit_exact(N, d, kernel):
     """Raw S_int read back from TMEM, every Q block against every key: N = 1024 / 2048 / 1900 run
-    8-16 KV tiles through the 3-stage ring (phases wrap), in both the v8 and the persistent v10
-    kernel (v10 carries its ring phases across work items)."""
+    8-16 KV tiles through the 3-stage ring (phases wrap)."""
     B, Hq, Hkv = 1, 2, 1
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=3)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
@@ -111,7 +110,7 @@ def test_s_int_bit_exact(N, d, kernel):
             assert np.array_equal(s[hq, 128 * i:128 * i + 128].astype(np.int64), ref), (hq, i)
 
 
-@pytest.mark.parametrize("kernel", ["v8", "v10"])
+@pytest.mark.parametrize("kernel", ["v8"])
 @pytest.mark.parametrize("N,d,kind", [(256, 64, "iid"), (384, 128, "structured"), (1000, 128, "structured"),
                                       (2048, 128, "iid"), (1500, 64, "structured")])
 def test_phat_codes(N, d, kind, kernel):
@@ -183,9 +182,9 @@ OUT_CASES = [
     (1, 2, 1, 1000, 128, False, "structured"),
     (1, 1, 1, 1, 64, False, "iid"),            # N = 1: O = V up to fp8 rounding
     (1, 1, 1, 129, 128, True, "iid"),
-    (1, 1, 1, 1, 128, False, "iid"),           # default path v10 (d=128 non-causal): N = 1
-    (1, 3, 1, 100, 128, False, "structured"),  # v10: one ragged tile, 3 items < 148 CTAs
-    (1, 2, 1, 8192, 128, False, "iid"),        # v10 at its largest default N (sampled blocks below)
+    (1, 1, 1, 1, 128, False, "iid"),           # default path (d=128 non-causal): N = 1
+    (1, 3, 1, 100, 128, False, "structured"),  # one ragged tile
+    (1, 2, 1, 8192, 128, False, "iid"),        # 64 KV tiles (sampled blocks below)
 ]
 
 
@@ -270,7 +269,7 @@ def test_accuracy_vs_fp32_attention():
         assert cs > min_cos, (kind, cs)
 
 
-@pytest.mark.parametrize("kernel", ["default", "v10", "v8", "v12"])
+@pytest.mark.parametrize("kernel", ["default", "v8", "v12", "one"])
 @pytest.mark.parametrize("d,causal,N", [(128, False, 384), (64, True, 384), (128, True, 300), (64, False, 200)])
 def test_kernel_variants(kernel, d, causal, N):
     """Every attention kernel the library dispatches to matches the oracle run with its b_kv (C-9).
@@ -294,55 +293,36 @@ def test_kernel_variants(kernel, d, causal, N):
 
 
 @pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(2, 40, 8, 600, 128, False), (2, 40, 8, 600, 128, True),
-                                                 (1, 64, 64, 1100, 64, True), (3, 30, 10, 1024, 128, False)])
-def test_persistent_v10_many_items(B, Hq, Hkv, N, d, causal):
-    """v10 (persistent: one CTA per SM looping over (pair, h_q, b) items, barrier phases carried across
-    items) with more items than SMs, so CTAs run 2-5 items each: bit-identical to v8 (same arithmetic,
-    different schedule) on the whole tensor, and the oracle on a sample of Q blocks spread over items."""
+                                                 (1, 64, 64, 1100, 64, False), (3, 30, 10, 1024, 128, False)])
+def test_shared_workspace_many_ctas(B, Hq, Hkv, N, d, causal):
+    """More CTAs than SMs (several waves); the prepared workspace is read-only for sage2_attention, so
+    a second launch on it, and two launches sharing it on two streams at once, give the same bits;
+    the oracle on a sample of Q blocks spread over the grid."""
     q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=21)
     ws = sage2.alloc_workspace(B, Hq, Hkv, N, d, causal=causal)
     sage2.prepare(qg, kg, vg, ws, causal=causal)
-    o10, o8 = torch.empty_like(qg), torch.empty_like(qg)
-    sage2.attention(o10, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
-    sage2.attention(o8, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v8")
+    o1 = torch.empty_like(qg)
+    sage2.attention(o1, ws, B, Hq, Hkv, N, d, causal=causal)
     torch.cuda.synchronize()
-    assert torch.equal(o10, o8), "v10 differs from v8"
-    # work counters are per launch (library pool, zeroed before the launch): a second launch on the
-    # same workspace (no prepare in between) covers every item again, and two launches sharing one
-    # prepared workspace on two streams at once do not interfere (the workspace is read-only)
-    o10b = torch.full_like(qg, float("nan"))
-    sage2.attention(o10b, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+    o2 = torch.full_like(qg, float("nan"))
+    sage2.attention(o2, ws, B, Hq, Hkv, N, d, causal=causal)
     torch.cuda.synchronize()
-    assert torch.equal(o10b, o8), "second v10 launch differs"
-    o10c, o10d = torch.full_like(qg, float("nan")), torch.full_like(qg, float("nan"))
+    assert torch.equal(o2, o1), "second launch differs"
+    o3, o4 = torch.full_like(qg, float("nan")), torch.full_like(qg, float("nan"))
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     s1.wait_stream(torch.cuda.current_stream())
     s2.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s1):
-        sage2.attention(o10c, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+        sage2.attention(o3, ws, B, Hq, Hkv, N, d, causal=causal)
     with torch.cuda.stream(s2):
-        sage2.attention(o10d, ws, B, Hq, Hkv, N, d, causal=causal, kernel="v10")
+        sage2.attention(o4, ws, B, Hq, Hkv, N, d, causal=causal)
     torch.cuda.synchronize()
-    assert torch.equal(o10c, o8) and torch.equal(o10d, o8), "concurrent v10 launches interfere"
+    assert torch.equal(o3, o1) and torch.equal(o4, o1), "concurrent launches on one workspace interfere"
     nT = (N + 127) // 128
     units = [(b, h, i) for b in range(B) for h in range(Hq) for i in range(nT)][::11]
-    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, OracleConfig(causal=causal), debug=True)
-    _compare_out(to_np16(o10).astype(np.float64), res, units, N)
-
-
-@pytest.mark.parametrize("int8,smooth_v", [(True, False), (False, True), (True, True)])
-def test_persistent_v10_variants_match_v8(int8, smooth_v):
-    """SageAttn2-8b and smooth V through v10 with more items than SMs (B*H_q*pairs = 2*48*3 = 288):
-    bitwise the v8 output (same arithmetic, persistent schedule)."""
-    B, Hq, Hkv, N, d = 2, 48, 16, 700, 128
-    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "structured", seed=31)
-    ws = sage2.alloc_workspace(B, Hq, Hkv, N, d)
-    sage2.prepare(qg, kg, vg, ws, int8=int8, smooth_v=smooth_v)
-    o10, o8 = torch.empty_like(qg), torch.empty_like(qg)
-    sage2.attention(o10, ws, B, Hq, Hkv, N, d, int8=int8, smooth_v=smooth_v, kernel="v10")
-    sage2.attention(o8, ws, B, Hq, Hkv, N, d, int8=int8, smooth_v=smooth_v, kernel="v8")
-    torch.cuda.synchronize()
-    assert torch.equal(o10, o8)
+    cfg = OracleConfig(causal=causal, kv_tile=kv_tile_for(N, d, causal))
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+    _compare_out(to_np16(o1).astype(np.float64), res, units, N)
 
 
 @pytest.mark.parametrize("N,d", [(256, 64), (384, 128), (200, 128)])

@@ -62,7 +62,7 @@ def test_no_cpu_fallback_without_gpu():
 def test_default_kernel_dispatch_rule():
     """Host-only query of the kernel sage2_attention runs (include/sage2.h sage2_attention_kernel):
     v12 for d = 64 non-causal, v8 otherwise (d = 128, causal, the carrier / granularity / single-level
-    variants); v10 only when asked for."""
+    variants)."""
     from paper_2411_10958_b200 import sage2
     ak = sage2.attention_kernel
     assert ak(4096, 128) == 8 and ak(8192, 128) == 8 and ak(200, 128) == 8
@@ -71,4 +71,4 @@ def test_default_kernel_dispatch_rule():
     assert ak(4096, 64, causal=True) == 8 and ak(4096, 64, qk_e4m3=True) == 8
     assert ak(4096, 64, kernel="v8") == 8 and ak(4096, 64, kernel="v12") == 12
     assert ak(4096, 128, qk_e4m3=True) == 8 and ak(4096, 128, gran="block") == 8
-    assert ak(32768, 128, kernel="v10") == 10 and ak(1024, 128, kernel="v8") == 8
+    assert ak(1024, 128, kernel="v8") == 8
