@@ -258,6 +258,25 @@ def test_errors():
         sage2.attn(q, k, k)                         # H_q % H_kv != 0
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,N,d,causal", [(3, 21845, 21845, 5, 64, False), (1, 65535, 5, 3, 128, True)])
+def test_max_heads(B, Hq, Hkv, N, d, causal):
+    """The largest grid the ABI accepts (B * H_q = 65535 query heads, tiny ragged N, GQA 13107:1)
+    runs and matches the oracle on sampled heads; one more head is rejected with EINVAL."""
+    q, k, v, qg, kg, vg = _inputs(B, Hq, Hkv, N, d, "iid", seed=77)
+    out = sage2.attn(qg, kg, vg, causal=causal)
+    torch.cuda.synchronize()
+    kv_tile = kv_tile_for(N, d, causal)
+    heads = sorted({(0, 0), (B - 1, Hq - 1), (B // 2, Hq // 2), (0, Hq - 1)})
+    units = [(b, h, 0) for b, h in heads]
+    res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units,
+                                   OracleConfig(causal=causal, kv_tile=kv_tile), debug=True)
+    _compare_out(to_np16(out).astype(np.float64), res, units, N)
+    assert torch.isfinite(out.float()).all()
+    big = torch.zeros((1, 65536, 1, 64), dtype=torch.float16, device="cuda")
+    with pytest.raises(sage2.Sage2Error):
+        sage2.attn(big, big, big)                   # B * H_q = 65536 > 65535
+
+
 def test_accuracy_vs_fp32_attention():
     """The paper's metrics against fp32 attention computed by torch (harness reference)."""
     B, H, N, d = 1, 4, 2048, 128
