@@ -313,6 +313,15 @@ def run_ours(args, world, rank, local):
     else:                  # flushed steps: the sum of the per-step event pairs (flush excluded)
         ms = sum(a.elapsed_time(c) for a, _, c in kev) / args.steps
     kms = statistics.mean(b.elapsed_time(c) for _, b, c in kev)
+    # accuracy of this workload's output against fp64 softmax attention (BASELINE metric "cos-sim vs
+    # FP32 attention"; the paper's metrics), outside every timed region: sampled heads / rows
+    acc = None
+    if rank == 0:
+        from paper_2411_10958_b200 import accuracy
+        heads = sorted({(0, 0), (lB - 1, lHq - 1)})
+        acc = accuracy.evaluate(out, q, k, v, causal, heads, accuracy.sample_rows(N, full_up_to=1024))
+        acc.update({"reference": "softmax attention in fp64", "heads": len(heads),
+                    "rows_per_head": int(accuracy.sample_rows(N, full_up_to=1024).numel())})
     prep_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in kev)
     ms_max = max_over_ranks(ms, world)
     kms_max = max_over_ranks(kms, world)
@@ -393,6 +402,8 @@ def run_ours(args, world, rank, local):
         "e2e": e2e,
         "phases_ms": {"preprocessing": prep_ms, "attention": kms},
     }
+    if acc is not None:
+        line["accuracy"] = acc
     line["roofline"].update(binding_roofs(achieved, d, clk.summary()))
     if validation is not None:
         line["validation"] = validation
