@@ -280,7 +280,11 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
 #pragma unroll
                     for (int c = 0; c < 64; c += 4) {
                         const uint32_t* rr = c < 32 ? r0 : r1;
+#ifdef SAGE2_ABL_NODS
+                        const float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);   // ablation build only
+#else
                         const float4 d4 = lds128(dss + 4 * c);
+#endif
                         const int g = (c % 8) / 2;
                         float2 sa2 = sc2[g], sb2 = sc2[g + 1];
                         if (GRAN == 2) {                     // one delta_K per key column
@@ -318,8 +322,12 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 const float mh = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
                 float* xmb = xm + (j & 1) * 256;
                 xmb[h * 128 + row] = mh;
+#ifdef SAGE2_ABL_NOXCHG
+                const float m_new = fmaxf(m, mh);                          // ablation build only
+#else
                 pair_sync();
                 const float m_new = fmax3(m, mh, xmb[(1 - h) * 128 + row]);
+#endif
                 const float alpha = (m == -INFINITY) ? 0.0f : ex2_approx(m - m_new);
                 const float m_use = (m_new == -INFINITY) ? 0.0f : (m_new - kLog2_448);
                 tss(j, 3);
@@ -401,6 +409,9 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
                 tss(j, 7);
                 if (TIMING && k == 0 && lane == 0) ts(4 + wq + 4 * h, j, 7);   // every warp's R read
                 const float2 a2 = make_float2(alpha, alpha);
+#ifdef SAGE2_ABL_NOPROMO
+                if (j == 0)                                                 // ablation build only
+#endif
 #pragma unroll
                 for (int c0 = 0; c0 < DH; c0 += 32) {
                     uint32_t o[32];
