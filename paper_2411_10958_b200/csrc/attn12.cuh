@@ -262,7 +262,11 @@ __global__ void __launch_bounds__(640, 1) k_attn12(const AttnParams p) {
 #pragma unroll
                     for (int c = 0; c < 64; c += 8) {
                         const uint32_t* rr = c < 32 ? r0 : r1;
+#ifdef SAGE2_ABL_NODS
+                        const float4 d0 = make_float4(0.f, 0.f, 0.f, 0.f), d1 = d0;   // ablation build only
+#else
                         const float4 d0 = lds128(dss + 4 * c), d1 = lds128(dss + 4 * c + 16);
+#endif
                         const float2 a = ffma2(make_float2((float)(int32_t)rr[c % 32], (float)(int32_t)rr[c % 32 + 1]), sc01,
                                                make_float2(d0.x, d0.y));
                         const float2 bq = ffma2(make_float2((float)(int32_t)rr[c % 32 + 2], (float)(int32_t)rr[c % 32 + 3]), sc23,
@@ -351,6 +355,9 @@ __global__ void __launch_bounds__(640, 1) k_attn12(const AttnParams p) {
                 tss(j, 7);
                 const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
+#ifdef SAGE2_ABL_NOPROMO
+                if (j == 0)                                                 // ablation build only
+#endif
                 for (int c0 = 0; c0 < 64; c0 += 32) {
                     uint32_t o[32];
                     if (j > 0) {
