@@ -109,6 +109,21 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * kStages2 + k); };
     auto bar_pa_full = [&](int k) { return bar0 + 8 * (9 + 2 * kStages2 + k); };   // first halves of P^
     auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
+    const size_t tile_bytes = (size_t)128 * D;
+    // producer: one K/V ring stage (K^, V^T, delta_K, the two tiles' Delta S rows)
+    auto load_stage = [&](int j, uint64_t keep) {
+        const int s = j % kStages2;
+        const uint32_t sa = stage_addr(s);
+        const bool d0 = j < nkv0, d1 = j < nkv1;
+        constexpr int NGK = gran_nk(GRAN);
+        mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 4 * NGK + 512 * (d0 + d1));
+        bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+        bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
+        bulk_g2s(sa + L::ST_DK, p.dk + ((size_t)bhk * nT + j) * NGK, 4 * NGK, bar_kv_full(s));
+        if (d0) bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+        if (d1) bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, bhq, it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+    };
+    const int jpre = nkv_max < kStages2 ? nkv_max : kStages2;   // stages issued before the CTA-wide sync
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -124,6 +139,13 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             mbar_init(bar_s_free(k), 256);
         }
         fence_mbar_init();
+        // the producer thread starts the Q and first K/V loads right away: their latency overlaps the
+        // TMEM allocation and the CTA-wide barrier (short sequences pay it once per few KV steps)
+        mbar_arrive_expect_tx(bar_q, L::TILE * ntiles);
+        bulk_g2s(sbase + L::Q0, p.qhat + ((size_t)bhq * nT + it0) * tile_bytes, L::TILE, bar_q);
+        if (ntiles == 2) bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)bhq * nT + it1) * tile_bytes, L::TILE, bar_q);
+        const uint64_t keep = policy_evict_last();
+        for (int j = 0; j < jpre; ++j) load_stage(j, keep);
     }
     // control warpgroup first (warps 0-3: producer, MMA issuers), softmax warpgroups 1-4 (measured
     // +1.5% against the control warps at the highest ids: the issuer hand-offs wake up sooner)
@@ -137,27 +159,12 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     if (wg == CW) {
         setmaxnreg_dec<32>();
         if (warp == 4 * CW && lane == 0) {
-            // ===================== producer =====================
-            const size_t tile_bytes = (size_t)128 * D;
-            mbar_arrive_expect_tx(bar_q, L::TILE * ntiles);
-            bulk_g2s(sbase + L::Q0, p.qhat + ((size_t)bhq * nT + it0) * tile_bytes, L::TILE, bar_q);
-            if (ntiles == 2)
-                bulk_g2s(sbase + L::Q1, p.qhat + ((size_t)bhq * nT + it1) * tile_bytes, L::TILE, bar_q);
+            // ===================== producer (the first jpre stages were issued before the sync) =====================
             const uint64_t keep = policy_evict_last();
-            for (int j = 0; j < nkv_max; ++j) {
+            for (int j = jpre; j < nkv_max; ++j) {
                 const int s = j % kStages2;
-                if (j >= kStages2) mbar_wait(bar_kv_empty(s), ((j / kStages2) - 1) & 1);
-                const uint32_t sa = stage_addr(s);
-                const bool d0 = j < nkv0, d1 = j < nkv1;
-                constexpr int NGK = gran_nk(GRAN);
-                mbar_arrive_expect_tx(bar_kv_full(s), 2 * L::TILE + 4 * NGK + 512 * (d0 + d1));
-                bulk_g2s_hint(sa + L::ST_K, p.khat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
-                bulk_g2s_hint(sa + L::ST_V, p.vhat + ((size_t)bhk * nT + j) * tile_bytes, L::TILE, bar_kv_full(s), keep);
-                bulk_g2s(sa + L::ST_DK, p.dk + ((size_t)bhk * nT + j) * NGK, 4 * NGK, bar_kv_full(s));
-                if (d0)
-                    bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
-                if (d1)
-                    bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, bhq, it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
+                mbar_wait(bar_kv_empty(s), ((j / kStages2) - 1) & 1);
+                load_stage(j, keep);
             }
         } else if (warp == 4 * CW + 1 || warp == 4 * CW + 2) {
             // ============ MMA issuer for Q tile k (whole warp converged, one elected lane issues) ============
