@@ -21,6 +21,9 @@
 namespace sage2 {
 
 constexpr int kTile = 128;  // b_q = b_kv = 128 tokens
+#ifndef SAGE2_STATS_U
+#define SAGE2_STATS_U 8   // k_kv_stats row passes in flight (4: C2-4K prepare 373 us, 8: 356, 12: 396 -- registers)
+#endif
 
 // Quantization granularity of Q and K (NEXT#4 ablation, oracle qk_gran): 0 per-thread (P:223,
 // SageAttn2), 1 per-block (Q: the 128-token block, K: 64-token blocks), 2 per-token, 3
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
                                                   unsigned long long* __restrict__ vsum) {
     constexpr int TPR = D / 8;          // threads per row
     constexpr int RPP = 256 / TPR;      // rows per pass
-    constexpr int U = 4;                // passes in flight
+    constexpr int U = SAGE2_STATS_U;    // passes in flight
     const int bh = blockIdx.y;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
