@@ -52,8 +52,8 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
     return ok != 0;
 }
 // Blocking wait with a watchdog: a protocol bug traps (launch error) instead of hanging the GPU.
-// (Measured: the suspend-hint variant below is neutral for v6 and 3% slower for v1 -- the spin
-// loop's issue slots are not what limits the softmax warps.)
+// (Measured: the suspend-hint variant below is 1-2% slower in the attention kernel's softmax and
+// MMA warps -- DESIGN.md section 9 -- the wake-up latency lands on the critical path.)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     // (A/B-measured against an asm spin loop whose first probe skips the compiler's YIELD: that
     // was 4% slower at d = 128 and 1-4% faster at d = 64; the C++ loop stays.)
