@@ -220,8 +220,9 @@ def run_reference(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / len(per),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
         "data": "synthetic", "config": workload_config(name),
-        "cpu_baseline": {"value": v, "unit": "TOPS", "cores": thr, "kind": "oracle",
-                         "sample": f"1 Q block (128 query rows x all {N} keys, its KV head preprocessed) per step"},
+        "cpu_baseline": {"value": v, "unit": "TOPS", "cores": thr, "kind": "oracle", "cpu": cpu_model(),
+                         "sample": f"1 Q block (128 query rows x all {N} keys, its KV head preprocessed) per step",
+                         "extrapolated_full_step_s": ops_of(B, Hq, N, d, causal) / (v * 1e12)},
         "e2e": {"value": v, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
