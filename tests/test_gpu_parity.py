@@ -516,6 +516,41 @@ def test_random_shapes_fuzz():
               f"int8={int8}: max|err|={err:.2e} cos={cos:.7f}")
 
 
+def test_random_variants_fuzz_long():
+    """Randomised longer sequences (2049..5000 tokens: the tensor-core Delta S, 17-40 KV tiles through
+    the ring) with the variant flags drawn too -- the E4M3 carrier, per-block / per-token / per-tensor
+    groups, the single-level ablation, INT8, smooth V, GQA, causal -- each against the oracle run with
+    the matching mode on sampled Q blocks (first, middle, last)."""
+    rng = np.random.default_rng(4242)
+    for case in range(10):
+        d = int(rng.choice([64, 128]))
+        Hkv = int(rng.integers(1, 3))
+        Hq = Hkv * int(rng.choice([1, 2, 4]))
+        N = int(rng.integers(2049, 5001))
+        causal = bool(rng.integers(0, 2))
+        kind = str(rng.choice(["iid", "structured"]))
+        variant = str(rng.choice(["default", "int8", "smooth_v", "carrier", "block", "token", "tensor", "one"]))
+        if variant in ("block", "token", "tensor"):
+            d = 128                                   # the granularity ablation is d = 128 only
+        kw = dict(int8=variant == "int8", smooth_v=variant == "smooth_v", qk_e4m3=variant == "carrier",
+                  gran=variant if variant in ("block", "token", "tensor") else "thread",
+                  kernel="one" if variant == "one" else "default")
+        q, k, v, qg, kg, vg = _inputs(1, Hq, Hkv, N, d, kind, seed=300 + case)
+        out = sage2.attn(qg, kg, vg, causal=causal, **kw)
+        torch.cuda.synchronize()
+        nT = (N + 127) // 128
+        units = [(0, h, i) for h in range(Hq) for i in sorted({0, nT // 2, nT - 1})]
+        cfg = OracleConfig(causal=causal, smooth_v=kw["smooth_v"], qk_max=127 if kw["int8"] else 7,
+                           smooth_q=not kw["int8"],
+                           qk_gran={"thread": 0, "block": 1, "token": 2, "tensor": 3}[kw["gran"]],
+                           two_level=variant != "one",
+                           kv_tile=kv_tile_for(N, d, causal, kernel=kw["kernel"], qk_e4m3=kw["qk_e4m3"], gran=kw["gran"]))
+        res = orc.sage2_forward_blocks(q.numpy(), k.numpy(), v.numpy(), units, cfg, debug=True)
+        err, cos, worst, used, rows = _compare_out(to_np16(out).astype(np.float64), res, units, N)
+        print(f"long case {case}: Hq={Hq} Hkv={Hkv} N={N} d={d} causal={causal} {kind} {variant}: "
+              f"max|err|={err:.2e} cos={cos:.7f} rows beyond the bar={used}/{rows}")
+
+
 @pytest.mark.parametrize("causal", [False, True])
 def test_delta_s_tensor_core_path(causal):
     """Delta S on the persistent tf32 tcgen05 GEMM (used for N > 2048; shorter sequences take the
