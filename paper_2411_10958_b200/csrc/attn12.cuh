@@ -60,6 +60,8 @@ struct Attn12Smem {
 
 template <bool CAUSAL, bool DUMP, bool TIMING = false>
 __global__ void __launch_bounds__(640, 1) k_attn12(const AttnParams p) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     constexpr int D = 64;
     using L = Attn12Smem;
     extern __shared__ uint8_t smem_raw[];

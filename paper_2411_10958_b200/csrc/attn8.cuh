@@ -57,6 +57,8 @@ struct Attn8Smem {
 // no longer shares its TMEM columns with R_k, so QK(j+1) is issued as soon as S(j) is in registers.
 template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false>
 __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     using L = Attn8Smem<D>;
     constexpr int DH = D / 2;                      // output channels per half
     extern __shared__ uint8_t smem_raw[];

@@ -47,6 +47,8 @@ template <int D>
 __global__ void __launch_bounds__(448, 1) k_delta_s_tc(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                        const uint8_t* __restrict__ qbt, int N, int Hq, int Hkv,
                                                        int BHq, float scale_log2, float* __restrict__ ds, int tri) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     // tri (causal workspaces): only query blocks i >= kt see key tile kt; rows are stored in the
     // compact triangular layout of ds_row() and items whose whole chunk lies above the diagonal are
     // skipped by every role alike (the same `live` predicate).

@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(256) k_kv_stats(const __half* __restrict__ K, 
                                                   int N, int rows_per_cta, unsigned long long* __restrict__ ksum,
                                                   unsigned int* __restrict__ vmax,
                                                   unsigned long long* __restrict__ vsum) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     constexpr int TPR = D / 8;          // threads per row
     constexpr int RPP = 256 / TPR;      // rows per pass
     constexpr int U = SAGE2_STATS_U;    // passes in flight
@@ -246,6 +248,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_v_absmax_smooth(const __half* __restrict__ V, int N, int rows_per_cta,
                                                          const unsigned long long* __restrict__ vsum,
                                                          unsigned int* __restrict__ vmax, float* __restrict__ vmean_out) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     constexpr int TPR = D / 8, RPP = 256 / TPR, U = 4;
     const int bh = blockIdx.y;
     const int lane = threadIdx.x % 32;
@@ -306,6 +310,8 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
                                                      float* __restrict__ dk, uint8_t* __restrict__ vhat,
                                                      float* __restrict__ kbar_out, float* __restrict__ dv_out,
                                                      const float* __restrict__ vmean, unsigned int* ktmax = nullptr) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     // ktmax (per-tensor granularity): GRAN 4 accumulates max|K'| of the head into ktmax[bh] and
     // stops; GRAN 3 then quantizes with delta_K = ktmax[bh] / qk_max for every group.
     constexpr int TPR = D / 8, RPP = 256 / TPR, NP = kTile / RPP;   // passes
@@ -453,6 +459,8 @@ __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q
                                                     int8_t* __restrict__ qhat, float* __restrict__ dq,
                                                     float* __restrict__ qbar_out, uint8_t* __restrict__ qbt,
                                                     unsigned int* qtmax = nullptr) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     // qtmax (per-tensor granularity): GRAN 4 accumulates max|gamma(Q_i)| of the head into qtmax[bh]
     // and stops (q_bar and its images are written as usual); GRAN 3 quantizes with
     // delta_Q = qtmax[bh] / qk_max.
@@ -589,6 +597,8 @@ template <int D>
 __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                  const float* __restrict__ qbar, int N, int Hq, int Hkv,
                                                  float scale_log2, float* __restrict__ ds, int tri) {
+    griddep_wait_and_release();   // PDL (ptx.cuh)
+
     constexpr int ICH = 32;                            // Q blocks per smem chunk
     const int kt = blockIdx.x, bhq = blockIdx.y, nT = gridDim.x, Np = nT * kTile;
     const int b = bhq / Hq, hq = bhq % Hq, hk = hq / (Hq / Hkv);

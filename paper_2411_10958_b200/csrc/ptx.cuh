@@ -340,6 +340,14 @@ __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads)
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Programmatic dependent launch (the prep kernels and the attention kernel are launched with
+// programmaticStreamSerialization): every kernel first waits for the grids it depends on to complete
+// and their writes to be visible, then lets its own dependent grid start launching (its CTAs take SMs
+// as this grid's last wave drains and then wait here in turn).  Both are no-ops without the attribute.
+__device__ __forceinline__ void griddep_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 // shared-memory vector load kept in program order (volatile: not hoisted across tcgen05 ops)
 __device__ __forceinline__ float4 lds128(uint32_t saddr) {
     float4 v;

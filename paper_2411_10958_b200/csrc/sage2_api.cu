@@ -177,6 +177,30 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
 }
 
 constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12;
+
+// Kernel launch with programmatic dependent launch (PDL): the kernel may start launching while the
+// previous kernel on the stream drains; every kernel of the library waits for its predecessor grid
+// at entry (griddep_wait_and_release, ptx.cuh), so the stream order of the data is unchanged.
+#ifndef SAGE2_NO_PDL
+#define SAGE2_PDL 1
+#else
+#define SAGE2_PDL 0
+#endif
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = SAGE2_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 constexpr int kGranFlags = SAGE2_F_GRAN_BLOCK | SAGE2_F_GRAN_TOKEN | SAGE2_F_GRAN_TENSOR;
 constexpr int kKnownFlags = SAGE2_F_CAUSAL | SAGE2_F_INT8 | SAGE2_F_DS_SIMT | SAGE2_F_QK_E4M3 | SAGE2_F_SMOOTH_V | SAGE2_F_ONE_LEVEL |
                             kGranFlags | kKernelFlags
@@ -239,10 +263,10 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     auto* vmean = reinterpret_cast<float*>(ws + L.off[R_VMEAN]);
     const dim3 sgrid((N + rows_per_cta - 1) / rows_per_cta, BHk);
     if (smv) {
-        k_kv_stats<D, true><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
-        k_v_absmax_smooth<D><<<sgrid, 256, 0, st>>>(v, N, rows_per_cta, vsum, vmax, vmean);
+        launch_k(k_kv_stats<D, true>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
+        launch_k(k_v_absmax_smooth<D>, sgrid, dim3(256), 0, st, v, N, rows_per_cta, vsum, vmax, vmean);
     } else {
-        k_kv_stats<D, false><<<sgrid, 256, 0, st>>>(k, v, N, rows_per_cta, ksum, vmax, vsum);
+        launch_k(k_kv_stats<D, false>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
     }
     const int gran = (flags & SAGE2_F_GRAN_TENSOR) ? 3 : (flags & SAGE2_F_GRAN_TOKEN) ? 2 : (flags & SAGE2_F_GRAN_BLOCK) ? 1 : 0;
     auto kvq = gran == 3 ? k_kv_quant<D, 3> : gran == 2 ? k_kv_quant<D, 2> : gran == 1 ? k_kv_quant<D, 1> : k_kv_quant<D, 0>;
@@ -260,20 +284,20 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     auto* dq_p = reinterpret_cast<float*>(ws + L.off[R_DQ]);
     auto* qbar_p = reinterpret_cast<float*>(ws + L.off[R_QBAR]);
     if (gran == 3) {
-        k_kv_quant<D, 4><<<dim3(nT, BHk), 256, 0, st>>>(k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
+        launch_k(k_kv_quant<D, 4>, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
                                                         kbar_p, dv_p, nullptr, ktmax);
-        k_q_quant<D, 4><<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT],
+        launch_k(k_q_quant<D, 4>, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT],
                                                        qtmax);
     }
-    kvq<<<dim3(nT, BHk), 256, 0, st>>>(k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p, dv_p,
+    launch_k(kvq, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p, dv_p,
                                        smv ? vmean : nullptr, ktmax);
-    qq<<<dim3(nT, BHq), 256, 0, st>>>(q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
+    launch_k(qq, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
     // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
     // oracle by the same bound.
     if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
-        k_delta_s<D><<<dim3(nT, BHq), 128, 0, st>>>(k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
+        launch_k(k_delta_s<D>, dim3(nT, BHq), dim3(128), 0, st, k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                     reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
                                                     scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
         return cuda_rc();
@@ -283,7 +307,7 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     if ((rc = configure_smem<k_delta_s_tc<D>>(DsgSmem<D>::ALLOC))) return rc;
     const long long items = (long long)BHq * nT * ((nT + 255) / 256);
     const int grid = (int)std::min<long long>(items, nsm);
-    k_delta_s_tc<D><<<grid, 448, DsgSmem<D>::ALLOC, st>>>(
+    launch_k(k_delta_s_tc<D>, dim3(grid), dim3(448), DsgSmem<D>::ALLOC, st,
         k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]), ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2,
         reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
     return cuda_rc();
@@ -294,7 +318,7 @@ int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn8Smem<D>::ALLOC;
     int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE>>(smem);
     if (rc) return rc;
-    k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE><<<dim3((p.nT + 1) / 2, p.Hq, B), 640, smem, st>>>(p);
+    launch_k(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE>, dim3((p.nT + 1) / 2, p.Hq, B), dim3(640), smem, st, p);
     return cuda_rc();
 }
 
@@ -303,7 +327,7 @@ int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     constexpr uint32_t smem = Attn12Smem::ALLOC;
     int rc = configure_smem<k_attn12<CAUSAL, DUMP, TIMING>>(smem);
     if (rc) return rc;
-    k_attn12<CAUSAL, DUMP, TIMING><<<dim3((p.nT + 3) / 4, p.Hq, B), 640, smem, st>>>(p);
+    launch_k(k_attn12<CAUSAL, DUMP, TIMING>, dim3((p.nT + 3) / 4, p.Hq, B), dim3(640), smem, st, p);
     return cuda_rc();
 }
 
