@@ -64,6 +64,10 @@ extern "C" {
 #define SAGE2_F_KERNEL_V12 131072 /* force the v12 kernel (csrc/attn12.cuh, d = 64 only: four Q tiles per  */
                                   /* CTA, b_kv = 64 -- the oracle's kv_tile is then 64, reading C-9).      */
                                   /* Not with QK_E4M3 / GRAN flags.                                       */
+#define SAGE2_F_KERNEL_V14 4194304 /* force the v14 kernel (csrc/attn14.cuh: one Q tile per CTA, S double- */
+                                  /* buffered, KV tiles alternating over two softmax pairs, promotion in  */
+                                  /* a correction warpgroup; b_kv = 128).  Non-causal; not with GRAN /     */
+                                  /* ONE_LEVEL flags.                                                     */
 #define SAGE2_F_ONE_LEVEL 1048576 /* ablation of the two-level accumulation (Table): the  */
                                   /* PV MMA accumulates into O in TMEM (O rescaled in place where the row */
                                   /* max moved); kernel v8 only.  Not the SageAttn2 default.              */

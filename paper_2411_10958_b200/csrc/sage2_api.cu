@@ -20,6 +20,7 @@
 
 #include "../../include/sage2.h"
 #include "attn12.cuh"
+#include "attn14.cuh"
 #include "attn8.cuh"
 #include "dsg.cuh"
 #include "prep.cuh"
@@ -176,7 +177,7 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12;
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12 | SAGE2_F_KERNEL_V14;
 
 // Kernel launch with programmatic dependent launch (PDL): the kernel may start launching while the
 // previous kernel on the stream drains; every kernel of the library waits for its predecessor grid
@@ -216,6 +217,8 @@ bool flags_ok(int flags) {
     // granularity ablation: v8 only; v12: kind::i8 codes only
     if ((flags & kGranFlags) && (flags & SAGE2_F_KERNEL_V12)) return false;
     if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_KERNEL_V12)) return false;
+    // v14: non-causal, two-level, per-thread granularity
+    if ((flags & SAGE2_F_KERNEL_V14) && (flags & (kGranFlags | SAGE2_F_ONE_LEVEL | SAGE2_F_CAUSAL))) return false;
     const int granf = kGranFlags;
     if ((flags & granf) & ((flags & granf) - 1)) return false;     // at most one granularity
     if ((flags & SAGE2_F_GRAN_TENSOR) && (flags & SAGE2_F_SMOOTH_V)) return false;   // shares vsum
@@ -232,6 +235,7 @@ bool flags_ok(int flags) {
 // kernel fixes the order of the keys inside the V^T tile images and Delta S rows).
 int kernel_of(int N, int d, int flags) {
     if (flags & SAGE2_F_KERNEL_V12) return 12;
+    if (flags & SAGE2_F_KERNEL_V14) return 14;
     if (flags & (SAGE2_F_KERNEL_V8 | SAGE2_F_ONE_LEVEL)) return 8;
     // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
     // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 of round 1 lost
@@ -331,6 +335,15 @@ int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+template <int D, bool QKF8, bool TIMING = false>
+int launch_attn14_t(const AttnParams& p, int B, cudaStream_t st) {
+    constexpr uint32_t smem = Attn14Smem<D>::ALLOC;
+    int rc = configure_smem<k_attn14<D, QKF8, TIMING>>(smem);
+    if (rc) return rc;
+    launch_k(k_attn14<D, QKF8, TIMING>, dim3(p.nT, p.Hq, B), dim3(640), smem, st, p);
+    return cuda_rc();
+}
+
 template <int D>
 int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStream_t st) {
     const bool causal = (flags & SAGE2_F_CAUSAL) != 0;
@@ -341,9 +354,13 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if constexpr (D == 64) {
             if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
         }
+        if (kern == 14) return launch_attn14_t<D, false, true>(p, B, st);
         return launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
 #endif
+    if (kern == 14 && !dump) {   // one Q tile per CTA, S double-buffered (DUMP builds: v8)
+        return f8 ? launch_attn14_t<D, true>(p, B, st) : launch_attn14_t<D, false>(p, B, st);
+    }
     if (kern == 12) {     // four Q tiles per CTA, b_kv = 64: head dim 64 only
         if constexpr (D != 64) {
             return SAGE2_EINVAL;

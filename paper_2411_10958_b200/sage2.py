@@ -140,7 +140,7 @@ def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=Fa
     qk_e4m3=True runs QK^T through the E4M3 carrier (kind::f8f6f4) instead of kind::i8;
     smooth_v=True subtracts V's column mean before the FP8 quantization and adds it back (P:304-306);
     gran="block"/"token" selects the granularity-ablation quantization groups (d = 128 only);
-    kernel forces an attention kernel / the single-level ablation ("v8", "v12", "one")."""
+    kernel forces an attention kernel / the single-level ablation ("v8", "v12", "v14", "one")."""
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     if out is None:
@@ -174,7 +174,7 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576}   # include/sage2.h SAGE2_F_KERNEL_*; "one": v8 single-level ablation
+KERNEL_FLAGS = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576, "v14": 4194304}   # include/sage2.h SAGE2_F_KERNEL_*; "one": v8 single-level ablation
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,

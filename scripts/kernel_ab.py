@@ -23,7 +23,7 @@ names = (sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] else "default").split(
 rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 B = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 H = int(sys.argv[6]) if len(sys.argv) > 6 else 32
-KF = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576}
+KF = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576, "v14": 4194304}
 q, k, v = synth.make_qkv(B, H, H, N, d, device="cuda")
 out = torch.empty_like(q)
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
