@@ -149,8 +149,8 @@ int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offse
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* Which attention kernel sage2_attention runs for (N, d, flags): 12 or 8 (SAGE2_F_KERNEL_V12 /
- * _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
+/* Which attention kernel sage2_attention runs for (N, d, flags): 14, 12 or 8 (SAGE2_F_KERNEL_V14 /
+ * _V12 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
  * non-causal, 8 otherwise).  Host-only, no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 

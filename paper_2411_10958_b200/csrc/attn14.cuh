@@ -16,8 +16,8 @@
 // CTA = 640 threads (20 warps):
 //   warp 0        producer: bulk-async copies of the pre-swizzled K^ / V^T tiles, Delta S row, delta_K
 //                 (NST-deep mbarrier ring, L2 evict-last)
-//   warp 1        MMA issuer (whole warp converged, elect.sync): S_{j%2} = Q^ K^_j^T (kind::i8, exact
-//                 s32), R = P^_j V^_j (kind::f8f6f4, fresh fp32 accumulator; tile 0 straight into O)
+//   warps 1, 2    MMA issuers (whole warp converged, elect.sync): S_{j%2} = Q^ K^_j^T (kind::i8, exact
+//                 s32) / R = P^_j V^_j (kind::f8f6f4, fresh fp32 accumulator; tile 0 straight into O)
 //   warps 4-19    softmax: pair P = tiles j = P (mod 2), key half h (columns [64h, 64h + 64)), thread =
 //                 (row, half): s = S dQ dK log2e/sqrt(d) + Delta S', exact row max through
 //                 shared memory, P^ = e4m3(2^(s - M_j + log2 448)) -> smem, partial row sums;
@@ -42,7 +42,7 @@ namespace sage2 {
 template <int D>
 struct Attn14Smem {
     static constexpr int NST = SAGE2_K14STAGES;              // K/V ring: tiles j, j+1, j+2 live + 1 prefetch
-    static constexpr int NM = 4;                            // running-max ring M_j -> pair of j+1
+    static constexpr int NM = 4;                            // running-max ring M_j -> pair of j+1 (8 with CORR)
     static constexpr uint32_t TILE = 128 * D;
     static constexpr uint32_t Q = 0;
     // stage: K^ | V^T | Delta S row (512 B) | delta_K (32 B)
@@ -50,24 +50,66 @@ struct Attn14Smem {
     static constexpr uint32_t STAGE = ((2 * TILE + 1024) + 1023) / 1024 * 1024;
     static constexpr uint32_t ST0 = TILE;
     static constexpr uint32_t P0 = ST0 + NST * STAGE;      // P^ of pair 0 / 1: 128 x 128 e4m3 (SW128)
-    static constexpr uint32_t MR = P0 + 2 * 16384;         // float M[NM][128]
-    static constexpr uint32_t XM = MR + NM * 128 * 4;      // float xm[2 pairs][2 buf][2 halves][128]
+    static constexpr uint32_t MR = P0 + 2 * 16384;         // float M[8][128]
+    static constexpr uint32_t XM = MR + 8 * 128 * 4;      // float xm[2 pairs][2 buf][2 halves][128]
     static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;   // float l[2 pairs][2 halves][128], m[2][128]
     static constexpr uint32_t BAR = XL + (2 * 2 * 128 + 2 * 128) * 4;
-    static constexpr uint32_t NBAR = 1 + 2 * NST + 2 + 2 + 2 + 2 + 1 + 1 + 2 + NM + 1;
+    static constexpr uint32_t NBAR = 1 + 2 * NST + 2 + 2 + 2 + 2 + 1 + 1 + 2 + 8 + 1;
     static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
     static constexpr uint32_t BYTES = TMEMPTR + 16;
     static constexpr uint32_t ALLOC = BYTES + 1024;
 };
 
+// Epilogue of one query row: NC output channels from TMEM (tO, consecutive columns) starting at channel
+// c_base: O / l (inv_l; l carries the 448 factor) * delta_V (+ V_m with smooth V) -> fp16.
+template <int D, int NC>
+__device__ __forceinline__ void epilogue14(const AttnParams& p, uint32_t tO, float inv_l, int b, int hq, int bhk, int grow,
+                                           int c_base) {
+    const float* dvp = p.dv + (size_t)bhk * D + c_base;
+    const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D + c_base : nullptr;
+    __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D + c_base;
+#pragma unroll
+    for (int c0 = 0; c0 < NC; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + c0, o);
+        tmem_wait_ld();
+        reg_dep32(o);
+        if (grow < p.N) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+                const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c));
+                const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c + 4));
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 m0 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c)) : z;
+                const float4 m1 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c + 4)) : z;
+                __half2 h0 = __floats2half2_rn(fmaf(__uint_as_float(o[c]) * inv_l, d0.x, m0.x),
+                                               fmaf(__uint_as_float(o[c + 1]) * inv_l, d0.y, m0.y));
+                __half2 h1 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 2]) * inv_l, d0.z, m0.z),
+                                               fmaf(__uint_as_float(o[c + 3]) * inv_l, d0.w, m0.w));
+                __half2 h2 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 4]) * inv_l, d1.x, m1.x),
+                                               fmaf(__uint_as_float(o[c + 5]) * inv_l, d1.y, m1.y));
+                __half2 h3 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 6]) * inv_l, d1.z, m1.z),
+                                               fmaf(__uint_as_float(o[c + 7]) * inv_l, d1.w, m1.w));
+                *reinterpret_cast<uint4*>(orow + c0 + c) =
+                    make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                               *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+            }
+        }
+    }
+}
+
 // TIMING builds (dev library): clock64 stamps of CTA (0,0,0) -> (uint64*)p.s_dump [who][j][slot]; who = pair
 // (its row-0 thread of half 0) or 2 (MMA issuer lane 0).
-template <int D, bool QKF8 = false, bool TIMING = false>
-__global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
+// CORR: the promotion and the epilogue run in a separate correction warpgroup (warps 4-7, thread = query
+// row, 768 threads: registers 24 / 72 / 96 for control / correction / softmax) instead of in the pair that
+// exponentiated the tile.
+template <int D, bool QKF8 = false, bool TIMING = false, bool CORR = false>
+__global__ void __launch_bounds__(CORR ? 768 : 640, 1) k_attn14(const AttnParams p) {
     griddep_wait_and_release();   // PDL (ptx.cuh)
 
     using L = Attn14Smem<D>;
-    constexpr int NST = L::NST, NM = L::NM;
+    constexpr int NST = L::NST, NM = CORR ? 8 : L::NM;
+    constexpr int SW0 = CORR ? 2 : 1;           // first softmax warpgroup
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* sgen = smem_raw + (sbase - smem_u32(smem_raw));
@@ -115,7 +157,7 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
         mbar_init(bar_q, 1);
         for (int s = 0; s < NST; ++s) {
             mbar_init(kv_full(s), 1);
-            mbar_init(kv_empty(s), 1);          // MMA commit after PV(j)
+            mbar_init(kv_empty(s), 2);          // commits after QK(j) and after PV(j)
         }
         for (int k = 0; k < 2; ++k) {
             mbar_init(s_full(k), 1);
@@ -125,7 +167,7 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
             mbar_init(pv_done(k), 1);
         }
         mbar_init(r_full, 1);
-        mbar_init(r_free, 256);
+        mbar_init(r_free, CORR ? 128 : 256);
         for (int k = 0; k < NM; ++k) mbar_init(m_full(k), 128);   // the half-0 threads of a pair
         mbar_init(o_full, 1);
         fence_mbar_init();
@@ -142,7 +184,8 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
     float* mring = reinterpret_cast<float*>(sgen + L::MR);
 
     if (wg == 0) {
-        setmaxnreg_dec<32>();
+        if constexpr (CORR) setmaxnreg_dec<24>();
+        else setmaxnreg_dec<32>();
         if (warp == 0 && lane == 0) {
             // ===================== producer =====================
             const uint64_t keep = policy_evict_last();
@@ -151,64 +194,128 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
                 mbar_wait(kv_empty(s), ((j / NST) - 1) & 1);
                 load_stage(j, keep);
             }
-        } else if (warp == 1) {
-            // ===================== MMA issuer =====================
+        } else if (warp == 1 || warp == 2) {
+            // ============ MMA issuers: warp 1 QK^T, warp 2 PV (issue blocks ~70-100 cycles per MMA, so one
+            // warp for both serialises them: PV(j) committed ~1500 cycles after P^(j), measured) ============
             constexpr uint32_t IDQK = QKF8 ? idesc_e4m3(128, 128) : idesc_i8(128, 128);
             constexpr uint32_t IDPV = idesc_e4m3(128, D);
-            const uint64_t qdesc = smem_desc<D>(sbase + L::Q);
-            const uint32_t tR = tmem + 256, tO = tmem + 256 + D;
-            mbar_wait(bar_q, 0);
-            auto issue_qk = [&](int j) {
-                const int s = j % NST;
-                mbar_wait(kv_full(s), (j / NST) & 1);
-                tc_fence_after();
-                const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K);
-                const uint32_t tS = tmem + 128 * (j & 1);
-#pragma unroll
-                for (int kk = 0; kk < D / 32; ++kk) {
-                    if (QKF8) mma_f8f6f4_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
-                    else mma_i8_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
-                }
-                mma_commit_w(s_full(j & 1));
-            };
-            issue_qk(0);
-            if (nkv > 1) issue_qk(1);
-            for (int j = 0; j < nkv; ++j) {
-                const int bb = j & 1, u = j >> 1, s = j % NST;
-                if (lane == 0) ts(2, j, 0);
-                if (j + 2 < nkv) {                         // S(j) is in the pair's registers
-                    mbar_wait(s_free(bb), u & 1);
+            if (warp == 1) {
+                const uint64_t qdesc = smem_desc<D>(sbase + L::Q);
+                mbar_wait(bar_q, 0);
+                for (int j = 0; j < nkv; ++j) {
+                    const int s = j % NST;
+                    if (j >= 2) mbar_wait(s_free(j & 1), ((j - 2) >> 1) & 1);   // S(j-2) in the pair's registers
+                    mbar_wait(kv_full(s), (j / NST) & 1);
                     if (lane == 0) ts(2, j, 1);
-                    issue_qk(j + 2);
+                    tc_fence_after();
+                    const uint64_t kdesc = smem_desc<D>(stage_addr(s) + L::ST_K);
+                    const uint32_t tS = tmem + 128 * (j & 1);
+#pragma unroll
+                    for (int kk = 0; kk < D / 32; ++kk) {
+                        if (QKF8) mma_f8f6f4_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                        else mma_i8_w(tS, qdesc + 2 * kk, kdesc + 2 * kk, IDQK, kk > 0);
+                    }
+                    mma_commit_w(s_full(j & 1));
+                    mma_commit_w(kv_empty(s));                // K^_j consumed
                     if (lane == 0) ts(2, j, 2);
                 }
-                const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
-                const uint64_t pdesc = smem_desc<128>(sbase + L::P0 + bb * 16384);
-                const uint32_t tD = j == 0 ? tO : tR;     // tile 0's R is O itself
-                // each key half's first 32 codes (K steps 0 and 2) go while the second 32 are exponentiated
-                mbar_wait(pa_full(bb), u & 1);
-                if (lane == 0) ts(2, j, 3);
-                if (j >= 2) mbar_wait(r_free, (j - 2) & 1);   // R(j-1) drained by its pair
-                if (lane == 0) ts(2, j, 4);
-                tc_fence_after();
-                mma_f8f6f4_w(tD, pdesc + 0, vdesc + 0, IDPV, 0);
-                mma_f8f6f4_w(tD, pdesc + 4, vdesc + 4, IDPV, 1);
-                mbar_wait(p_full(bb), u & 1);
-                if (lane == 0) ts(2, j, 5);
-                tc_fence_after();
-                mma_f8f6f4_w(tD, pdesc + 2, vdesc + 2, IDPV, 1);
-                mma_f8f6f4_w(tD, pdesc + 6, vdesc + 6, IDPV, 1);
-                if (j >= 1) mma_commit_w(r_full);
-                mma_commit_w(kv_empty(s));
-                mma_commit_w(pv_done(bb));
-                if (lane == 0) ts(2, j, 6);
+            } else {
+                const uint32_t tR = tmem + 256, tO = tmem + 256 + D;
+                for (int j = 0; j < nkv; ++j) {
+                    const int bb = j & 1, u = j >> 1, s = j % NST;
+                    if (lane == 0) ts(2, j, 0);
+                    const uint64_t vdesc = smem_desc<128>(stage_addr(s) + L::ST_V);
+                    const uint64_t pdesc = smem_desc<128>(sbase + L::P0 + bb * 16384);
+                    const uint32_t tD = j == 0 ? tO : tR;     // tile 0's R is O itself
+                    // each key half's first 32 codes (K steps 0 and 2) go while the second 32 are exponentiated
+                    mbar_wait(pa_full(bb), u & 1);
+                    if (lane == 0) ts(2, j, 3);
+                    if (j >= 2) mbar_wait(r_free, (j - 2) & 1);   // R(j-1) drained
+                    if (lane == 0) ts(2, j, 4);
+                    tc_fence_after();
+                    mma_f8f6f4_w(tD, pdesc + 0, vdesc + 0, IDPV, 0);
+                    mma_f8f6f4_w(tD, pdesc + 4, vdesc + 4, IDPV, 1);
+                    mbar_wait(p_full(bb), u & 1);
+                    if (lane == 0) ts(2, j, 5);
+                    tc_fence_after();
+                    mma_f8f6f4_w(tD, pdesc + 2, vdesc + 2, IDPV, 1);
+                    mma_f8f6f4_w(tD, pdesc + 6, vdesc + 6, IDPV, 1);
+                    if (j >= 1) mma_commit_w(r_full);
+                    mma_commit_w(kv_empty(s));                // V^_j consumed (and Delta S / delta_K: read before P^)
+                    mma_commit_w(pv_done(bb));
+                    if (lane == 0) ts(2, j, 6);
+                }
+                mma_commit_w(o_full);
             }
-            mma_commit_w(o_full);
         }
+    } else if (CORR && wg == 1) {
+        setmaxnreg_dec<72>();
+        // ============ correction: O = alpha_j O + R_j, then the epilogue ============
+        // M ring protocol: M_{j+1} is read BEFORE R(j) is released (r_free), and its slot is rewritten only
+        // with M_{j+9}, which needs PV(j+5) to have run, which needs R(j+3) drained -- so the read can never
+        // see a newer value and the m_full phase can never be ambiguous.
+        const int wq = warp & 3, row = 32 * wq + lane;
+        const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
+        const uint32_t tR = tmem + 256 + lane_off, tO = tmem + 256 + D + lane_off;
+        mbar_wait(m_full(0), 0);
+        float m_prev = mring[row], m_cur = m_prev;
+        if (nkv > 1) {
+            mbar_wait(m_full(1), 0);
+            m_cur = mring[128 + row];
+        }
+        for (int j = 1; j < nkv; ++j) {
+            const float alpha = (m_prev == -INFINITY) ? 0.0f : ex2_approx(m_prev - m_cur);
+            const float2 a2 = make_float2(alpha, alpha);
+            mbar_wait(r_full, (j - 1) & 1);
+            tc_fence_after();
+            float m_next = m_cur;
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+                if (c0 == D - 32 && j + 1 < nkv) {         // M_{j+1} before R(j) is released (see above)
+                    mbar_wait(m_full((j + 1) % NM), ((j + 1) / NM) & 1);
+                    m_next = mring[((j + 1) % NM) * 128 + row];
+                }
+                uint32_t r[32], o[32];
+                tmem_ld32(tR + c0, r);
+                tmem_ld32(tO + c0, o);
+                tmem_wait_ld();
+                reg_dep32(r);
+                reg_dep32(o);
+                if (c0 == D - 32) {                        // all of R(j) has been read
+                    tc_fence_before();
+                    mbar_arrive(r_free);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const float2 v = ffma2(a2, make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])),
+                                           make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
+                    o[c] = __float_as_uint(v.x);
+                    o[c + 1] = __float_as_uint(v.y);
+                }
+                tmem_st32(tO + c0, o);
+            }
+            tmem_wait_st();
+            m_prev = m_cur;
+            m_cur = m_next;
+        }
+        mbar_wait(o_full, 0);                              // the last PV has landed
+        tc_fence_after();
+        named_bar_sync(7, 640);                            // the four softmax partial sums are in smem
+        const float* xl = reinterpret_cast<const float*>(sgen + L::XL);
+        const float mf = m_cur;
+        float lsum = 0.0f;
+#pragma unroll
+        for (int PP = 0; PP < 2; ++PP) {
+            const float mp = xl[512 + PP * 128 + row];
+            const float f = (mp == -INFINITY) ? 0.0f : ex2_approx(mp - mf);
+            lsum += (xl[(2 * PP) * 128 + row] + xl[(2 * PP + 1) * 128 + row]) * f;
+        }
+        epilogue14<D, D>(p, tO, 1.0f / lsum, b, hq, bhk, it * 128 + row, 0);
     } else {
-        setmaxnreg_inc<112>();     // pool = 96 x 640 (launch): 128 x 32 + 512 x 112
+        if constexpr (CORR) setmaxnreg_inc<96>();   // pool = 80 x 768: 128 x 24 + 128 x 72 + 512 x 96
+        else setmaxnreg_inc<112>();                 // pool = 96 x 640 (launch): 128 x 32 + 512 x 112
         // ============ softmax: pair P (tiles j = P mod 2), key half h ============
-        const int P = (wg - 1) >> 1, h = (wg - 1) & 1;
+        const int P = (wg - SW0) >> 1, h = (wg - SW0) & 1;
         constexpr int DH = D / 2;
         auto turn_wait = [&]() { named_bar_sync(1 + P, 512); };
         auto turn_pass = [&]() { named_bar_arrive(1 + (1 - P), 512); };
@@ -339,7 +446,7 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
             if (j + 1 < nkv) turn_pass();               // the last tile keeps the turn (balanced protocol)
             l = alpha * l + ((rs2.x + rs2.y) + (rs2b.x + rs2b.y));
             m_run = m_new;
-            if (j == 0) continue;                        // PV(0) wrote O itself
+            if (CORR || j == 0) continue;                // PV(0) wrote O itself
             // ---- two-level promotion O = alpha_j O + R(j), in tile order ----
             mbar_wait(r_full, (j - 1) & 1);
             tss(j, 7);
@@ -375,53 +482,26 @@ __global__ void __launch_bounds__(640, 1) k_attn14(const AttnParams p) {
                 promo_pass();
             }
         }
-        // ---- epilogue (the pair holding the last tile): O / l / 448 * delta_V ----
+        // ---- epilogue (the pair holding the last tile, or the correction warpgroup): O / l / 448 * delta_V ----
         float* xl = reinterpret_cast<float*>(sgen + L::XL);
         xl[(2 * P + h) * 128 + row] = l;
         if (h == 0) xl[512 + P * 128 + row] = m_run;
-        named_bar_sync(7, 512);
-        if (P == ((nkv - 1) & 1)) {
-            if (nkv == 1) mbar_wait(o_full, 0);          // PV(0) wrote O
-            tc_fence_after();
-            const float mf = m_run;                      // M of the last tile = the final row max
-            float lsum = 0.0f;
+        if constexpr (CORR) {
+            named_bar_arrive(7, 640);
+        } else {
+            named_bar_sync(7, 512);
+            if (P == ((nkv - 1) & 1)) {
+                if (nkv == 1) mbar_wait(o_full, 0);      // PV(0) wrote O
+                tc_fence_after();
+                const float mf = m_run;                  // M of the last tile = the final row max
+                float lsum = 0.0f;
 #pragma unroll
-            for (int PP = 0; PP < 2; ++PP) {
-                const float mp = xl[512 + PP * 128 + row];
-                const float f = (mp == -INFINITY) ? 0.0f : ex2_approx(mp - mf);
-                lsum += (xl[(2 * PP) * 128 + row] + xl[(2 * PP + 1) * 128 + row]) * f;
-            }
-            const float inv_l = 1.0f / lsum;
-            const float* dvp = p.dv + (size_t)bhk * D + DH * h;
-            const float* vmp = p.vmean ? p.vmean + (size_t)bhk * D + DH * h : nullptr;   // smooth V
-            __half* orow = p.out + (((size_t)b * p.Hq + hq) * p.N + grow) * D + DH * h;
-#pragma unroll
-            for (int c0 = 0; c0 < DH; c0 += 32) {
-                uint32_t o[32];
-                tmem_ld32(tO + c0, o);
-                tmem_wait_ld();
-                reg_dep32(o);
-                if (grow < p.N) {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 8) {
-                        const float4 d0 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c));
-                        const float4 d1 = __ldg(reinterpret_cast<const float4*>(dvp + c0 + c + 4));
-                        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                        const float4 m0 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c)) : z;
-                        const float4 m1 = vmp ? __ldg(reinterpret_cast<const float4*>(vmp + c0 + c + 4)) : z;
-                        __half2 h0 = __floats2half2_rn(fmaf(__uint_as_float(o[c]) * inv_l, d0.x, m0.x),
-                                                       fmaf(__uint_as_float(o[c + 1]) * inv_l, d0.y, m0.y));
-                        __half2 h1 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 2]) * inv_l, d0.z, m0.z),
-                                                       fmaf(__uint_as_float(o[c + 3]) * inv_l, d0.w, m0.w));
-                        __half2 h2 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 4]) * inv_l, d1.x, m1.x),
-                                                       fmaf(__uint_as_float(o[c + 5]) * inv_l, d1.y, m1.y));
-                        __half2 h3 = __floats2half2_rn(fmaf(__uint_as_float(o[c + 6]) * inv_l, d1.z, m1.z),
-                                                       fmaf(__uint_as_float(o[c + 7]) * inv_l, d1.w, m1.w));
-                        *reinterpret_cast<uint4*>(orow + c0 + c) =
-                            make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                                       *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
-                    }
+                for (int PP = 0; PP < 2; ++PP) {
+                    const float mp = xl[512 + PP * 128 + row];
+                    const float f = (mp == -INFINITY) ? 0.0f : ex2_approx(mp - mf);
+                    lsum += (xl[(2 * PP) * 128 + row] + xl[(2 * PP + 1) * 128 + row]) * f;
                 }
+                epilogue14<D, DH>(p, tO, 1.0f / lsum, b, hq, bhk, grow, DH * h);
             }
         }
     }

@@ -335,12 +335,16 @@ int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+#ifndef SAGE2_V14_CORR
+#define SAGE2_V14_CORR 0   // the correction-warpgroup form measured slower
+#endif
 template <int D, bool QKF8, bool TIMING = false>
 int launch_attn14_t(const AttnParams& p, int B, cudaStream_t st) {
+    constexpr bool CORR = SAGE2_V14_CORR != 0;
     constexpr uint32_t smem = Attn14Smem<D>::ALLOC;
-    int rc = configure_smem<k_attn14<D, QKF8, TIMING>>(smem);
+    int rc = configure_smem<k_attn14<D, QKF8, TIMING, CORR>>(smem);
     if (rc) return rc;
-    launch_k(k_attn14<D, QKF8, TIMING>, dim3(p.nT, p.Hq, B), dim3(640), smem, st, p);
+    launch_k(k_attn14<D, QKF8, TIMING, CORR>, dim3(p.nT, p.Hq, B), dim3(CORR ? 768 : 640), smem, st, p);
     return cuda_rc();
 }
 

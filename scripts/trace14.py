@@ -3,7 +3,7 @@
 Pair P (row-0 thread of its half-0 warpgroup), per KV tile j, slots: 0 loop start, 1 S ready, 2 S loaded,
 3 dequant + partial max done, 4 max exchanged, 5 MUFU turn, 6 P^ written, 7 R ready, 8 previous
 promotion seen, 9 promotion done.  MMA issuer, per j: 0 loop, 1 s_free(j) seen, 2 QK(j+2) issued,
-3 first P^ half seen, 4 R free, 5 all of P^ seen, 6 PV(j) committed."""
+3 first P^ half seen, 4 R free, 5 all of P^ seen, 6 PV(j) committed (1, 2: the QK issuer: kv_full(j) seen, QK(j) committed)."""
 import os
 import sys
 
