@@ -322,17 +322,18 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     __shared__ float kbar[D], dvs[D];
     __shared__ __align__(16) __half vt[kTile * VS];
     const size_t base = (size_t)bh * N * D;
-    uint4 kraw[NP];
+    // every K and V load in flight first; k_bar / delta_V (fp64 and IEEE divisions) computed under
+    // their latency; then V is staged in shared memory (a store per load had each store wait out its
+    // own load: the round-1 kernel's top stall)
+    uint4 kraw[NP], vraw[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
         const int t = tile * kTile + p * RPP + rofs;
-        kraw[p] = make_uint4(0, 0, 0, 0);
-        uint4 vv = make_uint4(0, 0, 0, 0);
+        kraw[p] = vraw[p] = make_uint4(0, 0, 0, 0);
         if (t < N) {
             kraw[p] = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)t * D + cg * 8));
-            vv = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
+            vraw[p] = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
         }
-        *reinterpret_cast<uint4*>(&vt[(p * RPP + rofs) * VS + cg * 8]) = vv;
     }
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
@@ -343,6 +344,8 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
             dv_out[(size_t)bh * D + c] = dvs[c];
         }
     }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) *reinterpret_cast<uint4*>(&vt[(p * RPP + rofs) * VS + cg * 8]) = vraw[p];
     __syncthreads();
     // K' = K - k_bar (O-2), kept in registers; absmax per key row -> rowmax, then the group
     // absmax of the granularity (per-thread group g = rows 64(g/4) + 8k + 2(g%4) + {0, 1},
@@ -593,47 +596,83 @@ __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q
 //   ds[bh][i][t] = (log2(e)/sqrt(d)) * sum_c qbar_i[c] * (fp32(K[t,c]) - kbar[c])   (O-7)
 // fp32 FMA chain over c ascending.  Keys t >= N get 0 (masked in the kernel anyway).
 // ---------------------------------------------------------------------------------------------
-template <int D>
+template <int D, int NI = 16>
 __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, const float* __restrict__ kbar,
                                                  const float* __restrict__ qbar, int N, int Hq, int Hkv,
                                                  float scale_log2, float* __restrict__ ds, int tri) {
     griddep_wait_and_release();   // PDL (ptx.cuh)
 
-    constexpr int ICH = 32;                            // Q blocks per smem chunk
+    // Latency-lean form (the round-1 kernel held K' in 128 fp32 registers per thread -- 3 CTAs per SM --
+    // and made 128 scalar k_bar loads per thread: C2-1K 28 us): the key tile is staged in padded shared
+    // memory by coalesced loads (row stride D + 2 halves: thread t reads row t conflict-free), k_bar and
+    // q_bar come from shared memory, and NI Q blocks (the launch picks 8 or 16 for nT) are accumulated
+    // at once -- NI independent chains per thread.  Each output keeps its fp32 FMA chain over c ascending
+    // with K'[t,c] = fp32(K[t,c]) - k_bar[c] (O-2).
+    constexpr int KS = D + 2;                          // padded smem row (halves)
     const int kt = blockIdx.x, bhq = blockIdx.y, nT = gridDim.x, Np = nT * kTile;
     const int b = bhq / Hq, hq = bhq % Hq, hk = hq / (Hq / Hkv);
     const int bhk = b * Hkv + hk;
     const int t = kt * kTile + threadIdx.x;
-    __shared__ float sq[ICH][D];
-    float kp[D];
-    if (t < N) {
-        const __half* krow = K + ((size_t)bhk * N + t) * D;
+    __shared__ __align__(16) float sq[NI][D];
+    __shared__ __align__(16) float skb[D];
+    __shared__ __align__(16) __half sk[kTile * KS];
+    {
+        const __half* kt0 = K + ((size_t)bhk * N + (size_t)kt * kTile) * D;
+        constexpr int CPR = D / 8, NL = kTile * CPR / 128;   // 16-byte chunks per row / per thread
+        uint4 u[NL];                                   // every load in flight before the first store
 #pragma unroll
-        for (int c = 0; c < D; c += 8) {
-            uint4 u = __ldg(reinterpret_cast<const uint4*>(krow + c));
-            const __half* h = reinterpret_cast<const __half*>(&u);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) kp[c + i] = __fsub_rn(__half2float(h[i]), __ldg(kbar + (size_t)bhk * D + c + i));
+        for (int l = 0; l < NL; ++l) {
+            const int e = threadIdx.x + 128 * l, r = e / CPR, c8 = e % CPR;
+            u[l] = make_uint4(0, 0, 0, 0);
+            if (kt * kTile + r < N) u[l] = __ldg(reinterpret_cast<const uint4*>(kt0 + (size_t)r * D) + c8);
         }
-    } else {
 #pragma unroll
-        for (int c = 0; c < D; ++c) kp[c] = 0.0f;
+        for (int l = 0; l < NL; ++l) {
+            const int e = threadIdx.x + 128 * l, r = e / CPR, c8 = e % CPR;
+            uint32_t* dst = reinterpret_cast<uint32_t*>(&sk[r * KS + c8 * 8]);   // 4-byte aligned (KS even)
+            dst[0] = u[l].x;
+            dst[1] = u[l].y;
+            dst[2] = u[l].z;
+            dst[3] = u[l].w;
+        }
     }
+    if (threadIdx.x < D) skb[threadIdx.x] = kbar[(size_t)bhk * D + threadIdx.x];
+    const float live = t < N ? 1.0f : 0.0f;            // keys t >= N: 0 (masked in the kernel anyway)
+    const __half2* myk = reinterpret_cast<const __half2*>(&sk[threadIdx.x * KS]);
     const float* qb = qbar + (size_t)bhq * nT * D;
     // row offsets as ds_row() (common.cuh): full rows, or the causal triangular layout (i >= kt only)
     auto row = [&](int i) {
         return tri ? (size_t)bhq * 64 * (size_t)nT * (nT + 1) + 64 * (size_t)i * (i + 1) : ((size_t)bhq * nT + i) * Np;
     };
-    for (int i0 = tri ? (kt / ICH) * ICH : 0; i0 < nT; i0 += ICH) {
-        const int ni = min(ICH, nT - i0);
+    for (int i0 = tri ? (kt / NI) * NI : 0; i0 < nT; i0 += NI) {
+        const int ni = min(NI, nT - i0);
         __syncthreads();
-        for (int e = threadIdx.x; e < ni * D; e += 128) sq[e / D][e % D] = qb[(size_t)i0 * D + e];
+        for (int e = threadIdx.x; e < ni * D / 4; e += 128)
+            reinterpret_cast<float4*>(&sq[0][0])[e] = __ldg(reinterpret_cast<const float4*>(qb + (size_t)i0 * D) + e);
         __syncthreads();
-        for (int ii = 0; ii < ni; ++ii) {
-            float acc = 0.0f;
+        float acc[NI];
 #pragma unroll
-            for (int c = 0; c < D; ++c) acc = fmaf(sq[ii][c], kp[c], acc);
-            if (!tri || i0 + ii >= kt) ds[row(i0 + ii) + t] = acc * scale_log2;
+        for (int k = 0; k < NI; ++k) acc[k] = 0.f;
+#pragma unroll 4
+        for (int c = 0; c < D; c += 4) {
+            const float4 kb4 = *reinterpret_cast<const float4*>(&skb[c]);
+            const float2 f01 = __half22float2(myk[c / 2]);
+            const float2 f23 = __half22float2(myk[c / 2 + 1]);
+            const float k0 = __fsub_rn(f01.x, kb4.x) * live, k1 = __fsub_rn(f01.y, kb4.y) * live;
+            const float k2 = __fsub_rn(f23.x, kb4.z) * live, k3 = __fsub_rn(f23.y, kb4.w) * live;
+#pragma unroll
+            for (int k = 0; k < NI; ++k) {                    // rows >= ni hold stale values, never stored
+                const float4 qv = *reinterpret_cast<const float4*>(&sq[k][c]);
+                acc[k] = fmaf(qv.x, k0, acc[k]);
+                acc[k] = fmaf(qv.y, k1, acc[k]);
+                acc[k] = fmaf(qv.z, k2, acc[k]);
+                acc[k] = fmaf(qv.w, k3, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            const int i = i0 + k;
+            if (k < ni && (!tri || i >= kt)) ds[row(i) + t] = acc[k] * scale_log2;
         }
     }
 }

@@ -172,6 +172,24 @@ cudaMemPool_t lib_pool() {
     return g_pools[dev];
 }
 
+// Library-owned side stream per device: sage2_prepare runs the Q quantizer on it, concurrently with the
+// K/V statistics and quantizer on the caller's stream (fork / join through events recorded per call,
+// so concurrent calls on other streams stay ordered by their own events).  Null if creation failed:
+// the kernels then run in sequence on the caller's stream.
+std::mutex g_side_mu;
+cudaStream_t g_side[64] = {};
+
+cudaStream_t side_stream() {
+    int dev = 0;
+    if (current_device(&dev)) return nullptr;
+    std::lock_guard<std::mutex> g(g_side_mu);
+    if (!g_side[dev] && cudaStreamCreateWithFlags(&g_side[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        g_side[dev] = nullptr;
+    }
+    return g_side[dev];
+}
+
 cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     cudaMemPool_t pool = lib_pool();
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
@@ -257,21 +275,9 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     if (cudaMemsetAsync(ws + L.off[R_KSUM], 0, L.off[R_KBAR] - L.off[R_KSUM], st) != cudaSuccess) return cuda_rc();
     auto* ksum = reinterpret_cast<unsigned long long*>(ws + L.off[R_KSUM]);
     auto* vmax = reinterpret_cast<unsigned int*>(ws + L.off[R_VMAX]);
-    // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
-    // ~4 CTAs per SM (1K tokens: 22 -> ~10 us).  fp64 in-CTA sums stay exact up to 8192 rows.
-    int rows_per_cta = 512;
-    while (rows_per_cta > 64 && (long long)((N + rows_per_cta - 1) / rows_per_cta) * (long long)BHk < 4LL * 148)
-        rows_per_cta /= 2;
     const bool smv = (flags & SAGE2_F_SMOOTH_V) != 0;
     auto* vsum = reinterpret_cast<unsigned long long*>(ws + L.off[R_VSUM]);
     auto* vmean = reinterpret_cast<float*>(ws + L.off[R_VMEAN]);
-    const dim3 sgrid((N + rows_per_cta - 1) / rows_per_cta, BHk);
-    if (smv) {
-        launch_k(k_kv_stats<D, true>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
-        launch_k(k_v_absmax_smooth<D>, sgrid, dim3(256), 0, st, v, N, rows_per_cta, vsum, vmax, vmean);
-    } else {
-        launch_k(k_kv_stats<D, false>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
-    }
     const int gran = (flags & SAGE2_F_GRAN_TENSOR) ? 3 : (flags & SAGE2_F_GRAN_TOKEN) ? 2 : (flags & SAGE2_F_GRAN_BLOCK) ? 1 : 0;
     auto kvq = gran == 3 ? k_kv_quant<D, 3> : gran == 2 ? k_kv_quant<D, 2> : gran == 1 ? k_kv_quant<D, 1> : k_kv_quant<D, 0>;
     auto qq = gran == 3 ? k_q_quant<D, 3> : gran == 2 ? k_q_quant<D, 2> : gran == 1 ? k_q_quant<D, 1> : k_q_quant<D, 0>;
@@ -287,6 +293,36 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     auto* qhat_p = reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]);
     auto* dq_p = reinterpret_cast<float*>(ws + L.off[R_DQ]);
     auto* qbar_p = reinterpret_cast<float*>(ws + L.off[R_QBAR]);
+    // the Q quantizer depends on Q only: it runs on the side stream while the K/V kernels run here
+    // (all of them are latency-bound at short N); joined before Delta S, which
+    // needs q_bar and k_bar
+    cudaStream_t side = gran == 3 ? nullptr : side_stream();
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (side && (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                 cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
+                 cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_fork, 0) != cudaSuccess)) {
+        cudaGetLastError();
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        ev_fork = ev_join = nullptr;
+        side = nullptr;
+    }
+    if (side) {
+        launch_k(qq, dim3(nT, BHq), dim3(256), 0, side, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
+        if (cudaEventRecord(ev_join, side) != cudaSuccess) return cuda_rc();
+    }
+    // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
+    // ~4 CTAs per SM (1K tokens: 22 -> ~10 us).  fp64 in-CTA sums stay exact up to 8192 rows.
+    int rows_per_cta = 512;
+    while (rows_per_cta > 64 && (long long)((N + rows_per_cta - 1) / rows_per_cta) * (long long)BHk < 4LL * 148)
+        rows_per_cta /= 2;
+    const dim3 sgrid((N + rows_per_cta - 1) / rows_per_cta, BHk);
+    if (smv) {
+        launch_k(k_kv_stats<D, true>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
+        launch_k(k_v_absmax_smooth<D>, sgrid, dim3(256), 0, st, v, N, rows_per_cta, vsum, vmax, vmean);
+    } else {
+        launch_k(k_kv_stats<D, false>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
+    }
     if (gran == 3) {
         launch_k(k_kv_quant<D, 4>, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
                                                         kbar_p, dv_p, nullptr, ktmax);
@@ -295,13 +331,22 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     }
     launch_k(kvq, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p, dv_p,
                                        smv ? vmean : nullptr, ktmax);
-    launch_k(qq, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
+    if (side) {
+        const bool ok = cudaStreamWaitEvent(st, ev_join, 0) == cudaSuccess;
+        cudaEventDestroy(ev_fork);
+        cudaEventDestroy(ev_join);
+        if (!ok) return cuda_rc();
+    } else {
+        launch_k(qq, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
+    }
     const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
     // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
     // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
     // oracle by the same bound.
     if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
-        launch_k(k_delta_s<D>, dim3(nT, BHq), dim3(128), 0, st, k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
+        // Q blocks per pass sized to nT (8 / 16 accumulators per thread; more passes beyond 16 blocks)
+        auto kds = nT <= 8 ? k_delta_s<D, 8> : k_delta_s<D, 16>;
+        launch_k(kds, dim3(nT, BHq), dim3(128), 0, st, k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
                                                     reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
                                                     scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
         return cuda_rc();
