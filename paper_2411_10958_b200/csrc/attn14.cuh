@@ -33,6 +33,9 @@
 #include "prep.cuh"
 #include "ptx.cuh"
 
+#ifndef SAGE2_V14_CC
+#define SAGE2_V14_CC 16   // correction warpgroup chunk: 32 spills its 64 live values at 72 registers
+#endif
 #ifndef SAGE2_K14STAGES
 #define SAGE2_K14STAGES 4
 #endif
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(CORR ? 768 : 640, 1) k_attn14(const AttnParams
         }
     } else if (CORR && wg == 1) {
         setmaxnreg_dec<72>();
+        constexpr int CC = SAGE2_V14_CC;                  // promotion chunk (columns per TMEM round trip)
         // ============ correction: O = alpha_j O + R_j, then the epilogue ============
         // M ring protocol: M_{j+1} is read BEFORE R(j) is released (r_free), and its slot is rewritten only
         // with M_{j+9}, which needs PV(j+5) to have run, which needs R(j+3) drained -- so the read can never
@@ -270,29 +274,41 @@ __global__ void __launch_bounds__(CORR ? 768 : 640, 1) k_attn14(const AttnParams
             tc_fence_after();
             float m_next = m_cur;
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-                if (c0 == D - 32 && j + 1 < nkv) {         // M_{j+1} before R(j) is released (see above)
+            for (int c0 = 0; c0 < D; c0 += CC) {
+                if (c0 == D - CC && j + 1 < nkv) {         // M_{j+1} before R(j) is released (see above)
                     mbar_wait(m_full((j + 1) % NM), ((j + 1) / NM) & 1);
                     m_next = mring[((j + 1) % NM) * 128 + row];
                 }
-                uint32_t r[32], o[32];
+                uint32_t r[CC], o[CC];
+#if SAGE2_V14_CC == 32
                 tmem_ld32(tR + c0, r);
                 tmem_ld32(tO + c0, o);
                 tmem_wait_ld();
                 reg_dep32(r);
                 reg_dep32(o);
-                if (c0 == D - 32) {                        // all of R(j) has been read
+#else
+                tmem_ld16(tR + c0, r);
+                tmem_ld16(tO + c0, o);
+                tmem_wait_ld();
+                reg_dep16(r);
+                reg_dep16(o);
+#endif
+                if (c0 == D - CC) {                        // all of R(j) has been read
                     tc_fence_before();
                     mbar_arrive(r_free);
                 }
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
+                for (int c = 0; c < CC; c += 2) {
                     const float2 v = ffma2(a2, make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])),
                                            make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])));
                     o[c] = __float_as_uint(v.x);
                     o[c + 1] = __float_as_uint(v.y);
                 }
+#if SAGE2_V14_CC == 32
                 tmem_st32(tO + c0, o);
+#else
+                tmem_st16(tO + c0, o);
+#endif
             }
             tmem_wait_st();
             m_prev = m_cur;
