@@ -1,6 +1,7 @@
 """Small forward passes for compute-sanitizer (memcheck / racecheck / synccheck): config C1 and a
-ragged causal GQA case, through every product kernel (v8, v12, the single-level ablation) and
-the preprocessing kernels (SIMT and tensor-core Delta S).
+ragged causal GQA case, through every product kernel (v8, v12, the single-level ablation, the
+experimental v14) and the preprocessing kernels (SIMT and tensor-core Delta S, the side-stream Q
+quantizer of short sequences).
     compute-sanitizer --tool memcheck python scripts/sanitize_cases.py"""
 import os
 import sys
@@ -19,6 +20,9 @@ CASES = [  # B, Hq, Hkv, N, d, causal, kernel, extra prepare flags
     (1, 4, 2, 300, 128, True, "one", {}),
     (1, 2, 1, 2200, 128, False, "default", {}),          # tensor-core Delta S (N > 2048)
     (1, 2, 2, 333, 128, False, "default", {"smooth_v": True, "int8": True}),
+    (1, 2, 1, 700, 128, False, "v14", {}),               # v14 (experimental): 6 KV tiles, ragged
+    (1, 2, 2, 128, 128, False, "v14", {}),               # v14 with one KV tile (pair B idle)
+    (1, 2, 1, 333, 64, False, "v14", {"smooth_v": True}),
 ]
 for B, Hq, Hkv, N, d, causal, kern, fl in CASES:
     q, k, v = synth.make_qkv(B, Hq, Hkv, N, d, kind="structured", seed=2, device="cuda")
