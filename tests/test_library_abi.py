@@ -72,3 +72,5 @@ def test_default_kernel_dispatch_rule():
     assert ak(4096, 64, kernel="v8") == 8 and ak(4096, 64, kernel="v12") == 12
     assert ak(4096, 128, qk_e4m3=True) == 8 and ak(4096, 128, gran="block") == 8
     assert ak(1024, 128, kernel="v8") == 8
+    # the experimental v14 runs only when selected (csrc/attn14.cuh)
+    assert ak(4096, 128, kernel="v14") == 14 and ak(4096, 64, kernel="v14") == 14
