@@ -1,6 +1,6 @@
 // attn14.cuh -- SageAttention2 attention kernel v14 for sm_100a (Alg. 1 inner loop, PAPER.md:246-263;
 // b_kv = 128): ONE 128-row Q block per CTA, its KV tiles split over two softmax warpgroup PAIRS
-// (pair A: even tiles, pair B: odd tiles), S double-buffered in TMEM.
+// (pair A: even tiles, pair B: odd tiles), S double-buffered in TMEM.  Experimental (not the default).
 //
 // Why: in v8 the TMEM budget (two Q tiles x [S/R 128 + O 128 columns]) forces
 // R = P^V^ to be written over S, so QK(j+1) can only start once the softmax has read R(j) back; each
@@ -13,16 +13,22 @@
 // before tile j-1 is exponentiated, so the hand-off is off the MUFU path); the promotions
 // O = alpha_j O + R_j stay in tile order through a named-barrier hand-off.
 //
-// CTA = 640 threads (20 warps):
+// Two forms (template CORR; the library builds CORR = 1, SAGE2_V14_CORR in sage2_api.cu):
+//   CORR = 0, 640 threads (20 warps): the pair that exponentiated tile j also promotes R(j) and, for
+//             the last tile, runs the epilogue (warps 4-19 softmax);
+//   CORR = 1, 768 threads (24 warps): a correction warpgroup (warps 4-7, thread = query row, 16-column
+//             TMEM round trips) does every promotion and the epilogue; softmax warps 8-23.
 //   warp 0        producer: bulk-async copies of the pre-swizzled K^ / V^T tiles, Delta S row, delta_K
 //                 (NST-deep mbarrier ring, L2 evict-last)
 //   warps 1, 2    MMA issuers (whole warp converged, elect.sync): S_{j%2} = Q^ K^_j^T (kind::i8, exact
 //                 s32) / R = P^_j V^_j (kind::f8f6f4, fresh fp32 accumulator; tile 0 straight into O)
-//   warps 4-19    softmax: pair P = tiles j = P (mod 2), key half h (columns [64h, 64h + 64)), thread =
-//                 (row, half): s = S dQ dK log2e/sqrt(d) + Delta S', exact row max through
-//                 shared memory, P^ = e4m3(2^(s - M_j + log2 448)) -> smem, partial row sums;
-//                 then O = alpha_j O + R_j for output channels [hD/2, hD/2 + D/2) and, in the pair that
-//                 holds the last tile, the epilogue O / l / 448 * delta_V -> fp16
+//   softmax       pair P = tiles j = P (mod 2), key half h (columns [64h, 64h + 64)), thread = (row,
+//                 half): s = S dQ dK log2e/sqrt(d) + Delta S', exact row max through shared
+//                 memory, P^ = e4m3(2^(s - M_j + log2 448)) -> smem, partial row sums
+//   promotion     O = alpha_j O + R_j in tile order; epilogue O / l / 448 * delta_V
+//                 -> fp16
+// Measured slower than v8 in both forms; kept as the experimental selector
+// SAGE2_F_KERNEL_V14.
 // TMEM columns: S_0 [0,128) | S_1 [128,256) | R [256,256+D) | O [256+D,256+2D).
 #pragma once
 #include <cuda_fp16.h>
