@@ -20,7 +20,7 @@
 //       O in TMEM; epilogue O / l / 448 * delta_V -> fp16.
 //     The exp2 phases of the two Q tiles alternate (named barriers 1/2).
 // TMEM: S_k/R_k [128k, 128k + 128) (R written over S once both halves have read S), O_k
-// [256 + D k, +D).
+// [128 NT + D k, +D) (NT = Q tiles per CTA: 2, or 1 for short sequences -- two CTAs per SM).
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -32,18 +32,25 @@
 
 namespace sage2 {
 
-template <int D>
+#ifndef SAGE2_KSTAGES1
+#define SAGE2_KSTAGES1 2   // K/V ring depth of the one-tile form (two CTAs per SM must fit the 228 KB)
+#endif
+
+// NT = Q tiles per CTA: 2 (the default form) or 1 (short sequences: 256 TMEM columns and ~110 KB of
+// shared memory, so two CTAs share an SM and one's prologue / epilogue overlaps the other's loop).
+template <int D, int NT = 2>
 struct Attn8Smem {
     using B2 = PairSmem<D>;
+    static constexpr int KS = NT == 2 ? kStages2 : SAGE2_KSTAGES1;
     static constexpr uint32_t TILE = B2::TILE;
-    static constexpr uint32_t Q0 = B2::Q0, Q1 = B2::Q1;
+    static constexpr uint32_t Q0 = 0, Q1 = NT == 2 ? TILE : 0;
     static constexpr uint32_t ST_K = B2::ST_K, ST_V = B2::ST_V, ST_DS0 = B2::ST_DS0, ST_DS1 = B2::ST_DS1,
-                              ST_DK = B2::ST_DK, STAGE = B2::STAGE, ST0 = B2::ST0;
-    static constexpr uint32_t P0 = B2::P0, P1 = B2::P1;
-    static constexpr uint32_t XM = P1 + 16384;              // float xm[2 tiles][2 buf][2 halves][128]
-    static constexpr uint32_t XL = XM + 2 * 2 * 2 * 128 * 4;  // float xl[2 tiles][2 halves][128]
-    static constexpr uint32_t BAR = XL + 2 * 2 * 128 * 4;
-    static constexpr uint32_t NBAR = 1 + 2 * kStages2 + 10;
+                              ST_DK = B2::ST_DK, STAGE = B2::STAGE, ST0 = NT * TILE;
+    static constexpr uint32_t P0 = ST0 + KS * STAGE, P1 = NT == 2 ? P0 + 16384 : P0;
+    static constexpr uint32_t XM = P0 + NT * 16384;          // float xm[NT tiles][2 buf][2 halves][128]
+    static constexpr uint32_t XL = XM + NT * 2 * 2 * 128 * 4;  // float xl[NT tiles][2 halves][128]
+    static constexpr uint32_t BAR = XL + NT * 2 * 128 * 4;
+    static constexpr uint32_t NBAR = 1 + 2 * KS + 10;
     static constexpr uint32_t TMEMPTR = BAR + 8 * NBAR;
     static constexpr uint32_t BYTES = TMEMPTR + 16;
     static constexpr uint32_t ALLOC = BYTES + 1024;
@@ -55,11 +62,13 @@ struct Attn8Smem {
 // false): the PV MMA accumulates straight into O in TMEM (enable-input-D after the first key tile),
 // O is rescaled in place only in rows whose running max moved (alpha = 1 exactly otherwise), and S_k
 // no longer shares its TMEM columns with R_k, so QK(j+1) is issued as soon as S(j) is in registers.
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false>
-__global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false,
+          int NT = 2>
+__global__ void __launch_bounds__(NT == 2 ? 640 : 384, NT == 2 ? 1 : 2) k_attn8(const AttnParams p) {
     griddep_wait_and_release();   // PDL (ptx.cuh)
 
-    using L = Attn8Smem<D>;
+    using L = Attn8Smem<D, NT>;
+    constexpr int KST = L::KS;                     // K/V ring depth
     constexpr int DH = D / 2;                      // output channels per half
     extern __shared__ uint8_t smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -71,7 +80,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
     const int wg = warp / 4;
     const int nT = p.nT, Np = nT * 128;
-    const int npairs = (nT + 1) / 2;
+    const int npairs = NT == 2 ? (nT + 1) / 2 : nT;   // CTAs per head
     // causal: heavy Q-block pairs first, within each head (long sequences: a head's K/V stays in L2
     // while its CTAs run) or over all heads (p.lpt, short sequences: the tail wave holds only light
     // pairs -- C2-1K 456 -> 482, C2-4K 907 -> 932 TOPS in round 1)
@@ -86,7 +95,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     }
     const int bhq = b * p.Hq + hq;
     const int bhk = b * p.Hkv + hq / (p.Hq / p.Hkv);
-    const int it0 = 2 * pair, it1 = 2 * pair + 1;
+    const int it0 = NT * pair, it1 = NT == 2 ? it0 + 1 : nT;
     const int nkv0 = CAUSAL ? it0 + 1 : nT;
     const int nkv1 = (it1 < nT) ? (CAUSAL ? it1 + 1 : nT) : 0;
     const int nkv_max = nkv0 > nkv1 ? nkv0 : nkv1;
@@ -104,17 +113,17 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     const uint32_t bar0 = sbase + L::BAR;
     const uint32_t bar_q = bar0;
     auto bar_kv_full = [&](int s) { return bar0 + 8 * (1 + s); };
-    auto bar_kv_empty = [&](int s) { return bar0 + 8 * (1 + kStages2 + s); };
-    auto bar_s_full = [&](int k) { return bar0 + 8 * (1 + 2 * kStages2 + k); };
-    auto bar_p_full = [&](int k) { return bar0 + 8 * (3 + 2 * kStages2 + k); };
-    auto bar_r_full = [&](int k) { return bar0 + 8 * (5 + 2 * kStages2 + k); };
-    auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * kStages2 + k); };
-    auto bar_pa_full = [&](int k) { return bar0 + 8 * (9 + 2 * kStages2 + k); };   // first halves of P^
+    auto bar_kv_empty = [&](int s) { return bar0 + 8 * (1 + KST + s); };
+    auto bar_s_full = [&](int k) { return bar0 + 8 * (1 + 2 * KST + k); };
+    auto bar_p_full = [&](int k) { return bar0 + 8 * (3 + 2 * KST + k); };
+    auto bar_r_full = [&](int k) { return bar0 + 8 * (5 + 2 * KST + k); };
+    auto bar_s_free = [&](int k) { return bar0 + 8 * (7 + 2 * KST + k); };
+    auto bar_pa_full = [&](int k) { return bar0 + 8 * (9 + 2 * KST + k); };   // first halves of P^
     auto stage_addr = [&](int s) { return sbase + L::ST0 + s * L::STAGE; };
     const size_t tile_bytes = (size_t)128 * D;
     // producer: one K/V ring stage (K^, V^T, delta_K, the two tiles' Delta S rows)
     auto load_stage = [&](int j, uint64_t keep) {
-        const int s = j % kStages2;
+        const int s = j % KST;
         const uint32_t sa = stage_addr(s);
         const bool d0 = j < nkv0, d1 = j < nkv1;
         constexpr int NGK = gran_nk(GRAN);
@@ -125,13 +134,13 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
         if (d0) bulk_g2s(sa + L::ST_DS0, p.ds + ds_row(p.ds_tri, bhq, it0, nT) + (size_t)j * 128, 512, bar_kv_full(s));
         if (d1) bulk_g2s(sa + L::ST_DS1, p.ds + ds_row(p.ds_tri, bhq, it1, nT) + (size_t)j * 128, 512, bar_kv_full(s));
     };
-    const int jpre = nkv_max < kStages2 ? nkv_max : kStages2;   // stages issued before the CTA-wide sync
+    const int jpre = nkv_max < KST ? nkv_max : KST;   // stages issued before the CTA-wide sync
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
-        for (int s = 0; s < kStages2; ++s) {
+        for (int s = 0; s < KST; ++s) {
             mbar_init(bar_kv_full(s), 1);
-            mbar_init(bar_kv_empty(s), 2);      // one arrival per Q tile (MMA commit or bypass)
+            mbar_init(bar_kv_empty(s), NT);     // one arrival per Q tile (MMA commit or bypass)
         }
         for (int k = 0; k < 2; ++k) {
             mbar_init(bar_s_full(k), 1);
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     // control warpgroup first (warps 0-3: producer, MMA issuers), softmax warpgroups 1-4 (measured
     // +1.5% against the control warps at the highest ids: the issuer hand-offs wake up sooner)
     constexpr int CW = 0, SW0 = 1;
-    if (warp == 4 * CW) tmem_alloc<512>(sbase + L::TMEMPTR);
+    if (warp == 4 * CW) tmem_alloc<NT == 2 ? 512 : 256>(sbase + L::TMEMPTR);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -164,11 +173,11 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             // ===================== producer (the first jpre stages were issued before the sync) =====================
             const uint64_t keep = policy_evict_last();
             for (int j = jpre; j < nkv_max; ++j) {
-                const int s = j % kStages2;
-                mbar_wait(bar_kv_empty(s), ((j / kStages2) - 1) & 1);
+                const int s = j % KST;
+                mbar_wait(bar_kv_empty(s), ((j / KST) - 1) & 1);
                 load_stage(j, keep);
             }
-        } else if (warp == 4 * CW + 1 || warp == 4 * CW + 2) {
+        } else if (warp == 4 * CW + 1 || (NT == 2 && warp == 4 * CW + 2)) {
             // ============ MMA issuer for Q tile k (whole warp converged, one elected lane issues) ============
             const int k = warp - (4 * CW + 1);
             const int my_nkv = k ? nkv1 : nkv0;
@@ -177,11 +186,11 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             const uint64_t qdesc = smem_desc<D>(sbase + (k ? L::Q1 : L::Q0));
             const uint64_t pdesc = smem_desc<128>(sbase + (k ? L::P1 : L::P0));
             const uint32_t tS = tmem + 128 * k;
-            const uint32_t tPV = ONE ? tmem + 256 + D * k : tS;   // R over S (two-level) or O itself (ONE)
+            const uint32_t tPV = ONE ? tmem + 128 * NT + D * k : tS;   // R over S (two-level) or O itself (ONE)
             mbar_wait(bar_q, 0);
             for (int j = 0; j < nkv_max; ++j) {
-                const int s = j % kStages2;
-                mbar_wait(bar_kv_full(s), (j / kStages2) & 1);
+                const int s = j % KST;
+                mbar_wait(bar_kv_full(s), (j / KST) & 1);
                 if (lane == 0) ts(2 + k, j, 0);
                 if (j >= my_nkv) {                 // this tile is done: release the stage for it
                     if (lane == 0) mbar_arrive(bar_kv_empty(s));
@@ -224,12 +233,15 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             }
         }
     } else {
-        setmaxnreg_inc<112>();      // pool = 96 x 640 (launch): 32 + 4 x 112 = 5 x 96 (inc blocks otherwise)
+        // pool = 96 x 640 (launch): 32 + 4 x 112 = 5 x 96 (inc blocks otherwise); one-tile form: 80 x 384
+        if constexpr (NT == 2) setmaxnreg_inc<112>();
+        else setmaxnreg_inc<104>();
         // ============ softmax (key half h) + two-level promotion + epilogue for Q tile k ============
         const int k = (wg - SW0) >> 1, h = (wg - SW0) & 1;
         const int my_nkv = k ? nkv1 : nkv0, my_it = k ? it1 : it0;
-        auto turn_wait = [&]() { named_bar_sync(1 + k, 512); };
-        auto turn_pass = [&]() { named_bar_arrive(1 + (1 - k), 512); };
+        // the MUFU turns alternate between the two tiles of a CTA (no partner in the one-tile form)
+        auto turn_wait = [&]() { if (NT == 2) named_bar_sync(1 + k, 512); };
+        auto turn_pass = [&]() { if (NT == 2) named_bar_arrive(1 + (1 - k), 512); };
         auto pair_sync = [&]() { named_bar_sync(3 + k, 256); };   // the two halves of tile k
         if (k == 1) turn_pass();                    // tile 0 takes the first MUFU turn
         if (my_nkv > 0) {
@@ -238,7 +250,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             const uint32_t lane_off = (uint32_t)(32 * wq) << 16;
             const uint32_t tS = tmem + 128 * k + lane_off + 64 * h;      // this half's S columns
             const uint32_t tR = tmem + 128 * k + lane_off + DH * h;      // this half's R channels
-            const uint32_t tO = tmem + 256 + D * k + lane_off + DH * h;  // this half's O channels
+            const uint32_t tO = tmem + 128 * NT + D * k + lane_off + DH * h;  // this half's O channels
             const int grow = my_it * 128 + row;
             const float dqr = p.dq[((size_t)bhq * nT + my_it) * gran_nq(GRAN) +
                                    (GRAN == 2 ? row : GRAN == 1 ? 0 : 8 * (row / 32) + (row % 8))] * p.qk_scale_log2;
@@ -248,9 +260,9 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
             const bool tme = TIMING && h == 0 && row == 0;
             auto tss = [&](int j, int slot) { if (tme) ts(k, j, slot); };
             for (int j = 0; j < my_nkv; ++j) {
-                const int s = j % kStages2;
+                const int s = j % KST;
                 tss(j, 0);
-                mbar_wait(bar_kv_full(s), (j / kStages2) & 1);      // Delta S / delta_K landed
+                mbar_wait(bar_kv_full(s), (j / KST) & 1);      // Delta S / delta_K landed
                 mbar_wait(bar_s_full(k), j & 1);
                 tc_fence_after();
                 tss(j, 1);
@@ -494,7 +506,7 @@ __global__ void __launch_bounds__(640, 1) k_attn8(const AttnParams p) {
     __syncthreads();
     if (warp == 4 * CW) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc<NT == 2 ? 512 : 256>(tmem);
     }
 }
 

@@ -362,14 +362,19 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     return cuda_rc();
 }
 
-template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false>
+template <int D, bool CAUSAL, bool DUMP, bool QKF8 = false, bool TIMING = false, int GRAN = 0, bool ONE = false, int NT = 2>
 int launch_attn8_t(const AttnParams& p, int B, cudaStream_t st) {
-    constexpr uint32_t smem = Attn8Smem<D>::ALLOC;
-    int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE>>(smem);
+    constexpr uint32_t smem = Attn8Smem<D, NT>::ALLOC;
+    int rc = configure_smem<k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE, NT>>(smem);
     if (rc) return rc;
-    launch_k(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE>, dim3((p.nT + 1) / 2, p.Hq, B), dim3(640), smem, st, p);
+    launch_k(k_attn8<D, CAUSAL, DUMP, QKF8, TIMING, GRAN, ONE, NT>, dim3(NT == 2 ? (p.nT + 1) / 2 : p.nT, p.Hq, B),
+             dim3(NT == 2 ? 640 : 384), smem, st, p);
     return cuda_rc();
 }
+
+#ifndef SAGE2_NT1_MAX_TILES
+#define SAGE2_NT1_MAX_TILES 8   // v8 in its one-Q-tile form (two CTAs per SM) up to N = 1K
+#endif
 
 template <bool CAUSAL, bool DUMP, bool TIMING = false>
 int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
@@ -440,6 +445,9 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
     }
     if (dump) return f8 ? launch_attn8_t<D, false, true, true>(p, B, st) : launch_attn8_t<D, false, true>(p, B, st);
     if (f8) return causal ? launch_attn8_t<D, true, false, true>(p, B, st) : launch_attn8_t<D, false, false, true>(p, B, st);
+    if (p.nT <= SAGE2_NT1_MAX_TILES)   // short sequences: one Q tile per CTA, two CTAs per SM
+        return causal ? launch_attn8_t<D, true, false, false, false, 0, false, 1>(p, B, st)
+                      : launch_attn8_t<D, false, false, false, false, 0, false, 1>(p, B, st);
     return causal ? launch_attn8_t<D, true, false>(p, B, st) : launch_attn8_t<D, false, false>(p, B, st);
 }
 
