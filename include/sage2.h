@@ -155,7 +155,8 @@ int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, i
 
 /* Which attention kernel sage2_attention runs for (N, d, flags): 14, 12 or 8 (SAGE2_F_KERNEL_V14 /
  * _V12 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
- * non-causal, 8 otherwise).  Host-only, no CUDA call; never fails. */
+ * non-causal, 8 otherwise -- v8 runs one Q tile per CTA, two CTAs per SM, for N <= 1024).  Host-only,
+ * no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);
 
 /* Attention kernel only (Fig. 3 step 4, Alg. 1 lines P:246-263: S = psi^-1(Q^K^T) + Delta S,
