@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(256, 4) k_q_quant(const __half* __restrict__ Q
 // fp32 FMA chain over c ascending.  Keys t >= N get 0 (masked in the kernel anyway).
 // ---------------------------------------------------------------------------------------------
 template <int D, int NI = 16>
-__global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, const float* __restrict__ kbar,
+__global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, const unsigned long long* __restrict__ ksum,
                                                  const float* __restrict__ qbar, int N, int Hq, int Hkv,
                                                  float scale_log2, float* __restrict__ ds, int tri) {
     griddep_wait_and_release();   // PDL (ptx.cuh)
@@ -636,7 +636,9 @@ __global__ void __launch_bounds__(128) k_delta_s(const __half* __restrict__ K, c
             dst[3] = u[l].w;
         }
     }
-    if (threadIdx.x < D) skb[threadIdx.x] = kbar[(size_t)bhk * D + threadIdx.x];
+    // k_bar from k_kv_stats' exact sums (the same fixed_mean as k_kv_quant, O-1): Delta S needs only
+    // the statistics, so it runs concurrently with k_kv_quant (sage2_api.cu launch_prepare)
+    if (threadIdx.x < D) skb[threadIdx.x] = fixed_mean((long long)ksum[(size_t)bhk * D + threadIdx.x], N);
     const float live = t < N ? 1.0f : 0.0f;            // keys t >= N: 0 (masked in the kernel anyway)
     const __half2* myk = reinterpret_cast<const __half2*>(&sk[threadIdx.x * KS]);
     const float* qb = qbar + (size_t)bhq * nT * D;

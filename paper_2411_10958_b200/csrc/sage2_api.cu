@@ -293,24 +293,49 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     auto* qhat_p = reinterpret_cast<int8_t*>(ws + L.off[R_QHAT]);
     auto* dq_p = reinterpret_cast<float*>(ws + L.off[R_DQ]);
     auto* qbar_p = reinterpret_cast<float*>(ws + L.off[R_QBAR]);
-    // the Q quantizer depends on Q only: it runs on the side stream while the K/V kernels run here
-    // (all of them are latency-bound at short N); joined before Delta S, which
-    // needs q_bar and k_bar
+    // library side stream for the Q quantizer and Delta S (below); none for per-tensor granularity
     cudaStream_t side = gran == 3 ? nullptr : side_stream();
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // Delta S (needs q_bar and the K column sums, not k_kv_quant's outputs): the persistent tf32
+    // tensor-core GEMM, except for short sequences (N <= 2048) where its per-item pipeline overhead
+    // loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the oracle by the same bound
+    // (DESIGN.md section 5); the SIMT kernel takes k_bar from the exact sums itself (it may run before
+    // k_kv_quant), the GEMM the k_bar k_kv_quant wrote.
+    const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
+    auto launch_ds = [&](cudaStream_t s) -> int {
+        if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
+            // Q blocks per pass sized to nT (8 / 16 accumulators per thread; more passes beyond 16 blocks)
+            auto kds = nT <= 8 ? k_delta_s<D, 8> : k_delta_s<D, 16>;
+            launch_k(kds, dim3(nT, BHq), dim3(128), 0, s, k, ksum, reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq,
+                     Hkv, scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
+            return SAGE2_OK;
+        }
+        int nsm = 0, rc2 = sm_count(&nsm);
+        if (rc2) return rc2;
+        if ((rc2 = configure_smem<k_delta_s_tc<D>>(DsgSmem<D>::ALLOC))) return rc2;
+        const long long items = (long long)BHq * nT * ((nT + 255) / 256);
+        const int grid = (int)std::min<long long>(items, nsm);
+        // (after k_kv_quant: it reads the k_bar k_kv_quant wrote)
+        launch_k(k_delta_s_tc<D>, dim3(grid), dim3(448), DsgSmem<D>::ALLOC, s, k, reinterpret_cast<const float*>(kbar_p),
+                 ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]),
+                 causal ? 1 : 0);
+        return SAGE2_OK;
+    };
+    // Side stream (short sequences gain most: every kernel here is latency-bound at 1K-2K): the Q
+    // quantizer forked after the memset, then -- once k_kv_stats has the column sums, and for N <= 2048
+    // -- Delta S, concurrent with k_kv_stats / k_kv_quant on `st`; joined before Delta S otherwise.
+    cudaEvent_t ev_fork = nullptr, ev_stats = nullptr, ev_join = nullptr;
     if (side && (cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                 cudaEventCreateWithFlags(&ev_stats, cudaEventDisableTiming) != cudaSuccess ||
                  cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess ||
                  cudaEventRecord(ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_fork, 0) != cudaSuccess)) {
         cudaGetLastError();
         if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_stats) cudaEventDestroy(ev_stats);
         if (ev_join) cudaEventDestroy(ev_join);
-        ev_fork = ev_join = nullptr;
+        ev_fork = ev_stats = ev_join = nullptr;
         side = nullptr;
     }
-    if (side) {
-        launch_k(qq, dim3(nT, BHq), dim3(256), 0, side, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
-        if (cudaEventRecord(ev_join, side) != cudaSuccess) return cuda_rc();
-    }
+    if (side) launch_k(qq, dim3(nT, BHq), dim3(256), 0, side, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
     // rows per k_kv_stats CTA: 512 for long sequences; fewer for short ones so the grid still has
     // ~4 CTAs per SM (1K tokens: 22 -> ~10 us).  fp64 in-CTA sums stay exact up to 8192 rows.
     int rows_per_cta = 512;
@@ -323,6 +348,19 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     } else {
         launch_k(k_kv_stats<D, false>, sgrid, dim3(256), 0, st, k, v, N, rows_per_cta, ksum, vmax, vsum);
     }
+    // Delta S joins the side stream only in its SIMT form (N <= 2048: C2-1K prepare 92 -> 83 us); the
+    // persistent tensor-core GEMM (one 197 KB CTA per SM) loses its SMs to k_kv_quant when the two run
+    // together (4K 343 -> 352 us, 32K 3.24 -> 3.44 ms), so it runs after the join
+    const bool ds_side = side && ((flags & SAGE2_F_DS_SIMT) || N <= 2048);
+    if (side) {
+        if (ds_side) {
+            if (cudaEventRecord(ev_stats, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_stats, 0) != cudaSuccess)
+                return cuda_rc();
+            int rc2 = launch_ds(side);
+            if (rc2) return rc2;
+        }
+        if (cudaEventRecord(ev_join, side) != cudaSuccess) return cuda_rc();
+    }
     if (gran == 3) {
         launch_k(k_kv_quant<D, 4>, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
                                                         kbar_p, dv_p, nullptr, ktmax);
@@ -334,31 +372,18 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     if (side) {
         const bool ok = cudaStreamWaitEvent(st, ev_join, 0) == cudaSuccess;
         cudaEventDestroy(ev_fork);
+        cudaEventDestroy(ev_stats);
         cudaEventDestroy(ev_join);
         if (!ok) return cuda_rc();
-    } else {
-        launch_k(qq, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
-    }
-    const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)D));
-    // Delta S: the persistent tf32 tensor-core GEMM, except for short sequences (N <= 2048) where its
-    // per-item pipeline overhead loses to the SIMT kernel (1K: 40 vs 28 us).  Both are pinned to the
-    // oracle by the same bound.
-    if ((flags & SAGE2_F_DS_SIMT) || N <= 2048) {
-        // Q blocks per pass sized to nT (8 / 16 accumulators per thread; more passes beyond 16 blocks)
-        auto kds = nT <= 8 ? k_delta_s<D, 8> : k_delta_s<D, 16>;
-        launch_k(kds, dim3(nT, BHq), dim3(128), 0, st, k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]),
-                                                    reinterpret_cast<const float*>(ws + L.off[R_QBAR]), N, Hq, Hkv,
-                                                    scale_log2, reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
+        if (!ds_side) {
+            int rc2 = launch_ds(st);
+            if (rc2) return rc2;
+        }
         return cuda_rc();
     }
-    int nsm = 0, rc = sm_count(&nsm);
-    if (rc) return rc;
-    if ((rc = configure_smem<k_delta_s_tc<D>>(DsgSmem<D>::ALLOC))) return rc;
-    const long long items = (long long)BHq * nT * ((nT + 255) / 256);
-    const int grid = (int)std::min<long long>(items, nsm);
-    launch_k(k_delta_s_tc<D>, dim3(grid), dim3(448), DsgSmem<D>::ALLOC, st,
-        k, reinterpret_cast<const float*>(ws + L.off[R_KBAR]), ws + L.off[R_QBT], N, Hq, Hkv, (int)BHq, scale_log2,
-        reinterpret_cast<float*>(ws + L.off[R_DS]), causal ? 1 : 0);
+    launch_k(qq, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT], qtmax);
+    int rc3 = launch_ds(st);
+    if (rc3) return rc3;
     return cuda_rc();
 }
 
