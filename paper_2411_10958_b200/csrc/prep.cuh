@@ -302,7 +302,9 @@ __global__ void __launch_bounds__(256) k_v_absmax_smooth(const __half* __restric
 //                    in padded shared memory and read back column-wise (thread = channel pair)
 //   dk             : 8 groups per tile (g_K = 4*(t/64) + (t%8)/2)
 // ---------------------------------------------------------------------------------------------
-template <int D, int GRAN = 0>
+// PART: 3 = K and V (one launch), 1 = K only, 2 = V only (short sequences run the two halves as
+// concurrent launches on two streams, sage2_api.cu launch_prepare).
+template <int D, int GRAN = 0, int PART = 3>
 __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ K, const __half* __restrict__ V,
                                                      int N, int qk_max, int e4m3_codes,
                                                      const unsigned long long* __restrict__ ksum,
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
     const int lane = threadIdx.x % 32;
     const int cg = threadIdx.x % TPR, rofs = threadIdx.x / TPR;
     __shared__ float kbar[D], dvs[D];
-    __shared__ __align__(16) __half vt[kTile * VS];
+    __shared__ __align__(16) __half vt[(PART & 2) ? kTile * VS : 8];
     const size_t base = (size_t)bh * N * D;
     // every K and V load in flight first; k_bar / delta_V (fp64 and IEEE divisions) computed under
     // their latency; then V is staged in shared memory (a store per load had each store wait out its
@@ -331,22 +333,25 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
         const int t = tile * kTile + p * RPP + rofs;
         kraw[p] = vraw[p] = make_uint4(0, 0, 0, 0);
         if (t < N) {
-            kraw[p] = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)t * D + cg * 8));
-            vraw[p] = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
+            if (PART & 1) kraw[p] = __ldg(reinterpret_cast<const uint4*>(K + base + (size_t)t * D + cg * 8));
+            if (PART & 2) vraw[p] = __ldg(reinterpret_cast<const uint4*>(V + base + (size_t)t * D + cg * 8));
         }
     }
     if (threadIdx.x < D) {
         const int c = threadIdx.x;
-        kbar[c] = fixed_mean((long long)ksum[(size_t)bh * D + c], N);                 // O-1
-        dvs[c] = __fdiv_rn(__uint_as_float(vmax[(size_t)bh * D + c]), 448.0f);      // O-4
+        if (PART & 1) kbar[c] = fixed_mean((long long)ksum[(size_t)bh * D + c], N);                 // O-1
+        if (PART & 2) dvs[c] = __fdiv_rn(__uint_as_float(vmax[(size_t)bh * D + c]), 448.0f);      // O-4
         if (tile == 0) {
-            kbar_out[(size_t)bh * D + c] = kbar[c];
-            dv_out[(size_t)bh * D + c] = dvs[c];
+            if (PART & 1) kbar_out[(size_t)bh * D + c] = kbar[c];
+            if (PART & 2) dv_out[(size_t)bh * D + c] = dvs[c];
         }
     }
+    if constexpr ((PART & 2) != 0) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) *reinterpret_cast<uint4*>(&vt[(p * RPP + rofs) * VS + cg * 8]) = vraw[p];
+        for (int p = 0; p < NP; ++p) *reinterpret_cast<uint4*>(&vt[(p * RPP + rofs) * VS + cg * 8]) = vraw[p];
+    }
     __syncthreads();
+    if constexpr ((PART & 1) != 0) {
     // K' = K - k_bar (O-2), kept in registers; absmax per key row -> rowmax, then the group
     // absmax of the granularity (per-thread group g = rows 64(g/4) + 8k + 2(g%4) + {0, 1},
     // "K[8k+2i] together with K[8k+2i+1]")
@@ -411,6 +416,8 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
         const float delta = gdelta[GRAN == 3 ? 0 : GRAN == 2 ? r : GRAN == 1 ? r / 64 : 4 * (r / 64) + (r % 8) / 2];
         *reinterpret_cast<uint2*>(kimg + swz_off<D>(r, cg * 8)) = quant_pack8(kx[p], delta, qk_max, e4m3_codes != 0);
     }
+    }
+    if constexpr ((PART & 2) != 0) {
     // V codes (O-4): thread = channel pair (c, c+1) x TOK consecutive tokens -> V^T rows c, c+1
     constexpr int NPAIR = D / 2, TOK = kTile / (256 / NPAIR);
     const int cp = threadIdx.x % NPAIR, t0 = (threadIdx.x / NPAIR) * TOK, c = 2 * cp;
@@ -442,6 +449,7 @@ __global__ void __launch_bounds__(256, 3) k_kv_quant(const __half* __restrict__ 
         }
         *reinterpret_cast<uint4*>(vimg + swz_off<128>(c, t0 + tb)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
         *reinterpret_cast<uint4*>(vimg + swz_off<128>(c + 1, t0 + tb)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    }
     }
 }
 

@@ -177,17 +177,17 @@ cudaMemPool_t lib_pool() {
 // so concurrent calls on other streams stay ordered by their own events).  Null if creation failed:
 // the kernels then run in sequence on the caller's stream.
 std::mutex g_side_mu;
-cudaStream_t g_side[64] = {};
+cudaStream_t g_side[64][2] = {};
 
-cudaStream_t side_stream() {
+cudaStream_t side_stream(int i = 0) {
     int dev = 0;
     if (current_device(&dev)) return nullptr;
     std::lock_guard<std::mutex> g(g_side_mu);
-    if (!g_side[dev] && cudaStreamCreateWithFlags(&g_side[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    if (!g_side[dev][i] && cudaStreamCreateWithFlags(&g_side[dev][i], cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
-        g_side[dev] = nullptr;
+        g_side[dev][i] = nullptr;
     }
-    return g_side[dev];
+    return g_side[dev][i];
 }
 
 cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
@@ -352,6 +352,15 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     // persistent tensor-core GEMM (one 197 KB CTA per SM) loses its SMs to k_kv_quant when the two run
     // together (4K 343 -> 352 us, 32K 3.24 -> 3.44 ms), so it runs after the join
     const bool ds_side = side && ((flags & SAGE2_F_DS_SIMT) || N <= 2048);
+    // short sequences also split k_kv_quant into its K and V halves on two streams (a second side
+    // stream takes the K half), each CTA's serial load / reduce / quantize phases halved
+    cudaStream_t side2 = ds_side ? side_stream(1) : nullptr;
+    cudaEvent_t ev_join2 = nullptr;
+    if (side2 && cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        ev_join2 = nullptr;
+        side2 = nullptr;
+    }
     if (side) {
         if (ds_side) {
             if (cudaEventRecord(ev_stats, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_stats, 0) != cudaSuccess)
@@ -361,14 +370,28 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
         }
         if (cudaEventRecord(ev_join, side) != cudaSuccess) return cuda_rc();
     }
+    if (side2) {
+        if (cudaStreamWaitEvent(side2, ev_stats, 0) != cudaSuccess) return cuda_rc();
+        auto kq = gran == 2 ? k_kv_quant<D, 2, 1> : gran == 1 ? k_kv_quant<D, 1, 1> : k_kv_quant<D, 0, 1>;
+        launch_k(kq, dim3(nT, BHk), dim3(256), 0, side2, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
+                 kbar_p, dv_p, smv ? vmean : nullptr, ktmax);
+        if (cudaEventRecord(ev_join2, side2) != cudaSuccess) return cuda_rc();
+        auto vq = gran == 2 ? k_kv_quant<D, 2, 2> : gran == 1 ? k_kv_quant<D, 1, 2> : k_kv_quant<D, 0, 2>;
+        launch_k(vq, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
+                 kbar_p, dv_p, smv ? vmean : nullptr, ktmax);
+        const bool ok = cudaStreamWaitEvent(st, ev_join2, 0) == cudaSuccess;
+        cudaEventDestroy(ev_join2);
+        if (!ok) return cuda_rc();
+    }
     if (gran == 3) {
         launch_k(k_kv_quant<D, 4>, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT],
                                                         kbar_p, dv_p, nullptr, ktmax);
         launch_k(k_q_quant<D, 4>, dim3(nT, BHq), dim3(256), 0, st, q, N, qk_max, e4, smooth_q, qhat_p, dq_p, qbar_p, ws + L.off[R_QBT],
                                                        qtmax);
     }
-    launch_k(kvq, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p, dv_p,
-                                       smv ? vmean : nullptr, ktmax);
+    if (!side2)
+        launch_k(kvq, dim3(nT, BHk), dim3(256), 0, st, k, v, N, qk_max, e4, ksum, vmax, khat_p, dk_p, ws + L.off[R_VHAT], kbar_p,
+                 dv_p, smv ? vmean : nullptr, ktmax);
     if (side) {
         const bool ok = cudaStreamWaitEvent(st, ev_join, 0) == cudaSuccess;
         cudaEventDestroy(ev_fork);
