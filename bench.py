@@ -395,8 +395,8 @@ def run_ours(args, world, rank, local):
         "scaling": args.scaling, "vs_baseline": None, "dtype": "int4-in-int8 (QK^T) + e4m3 (PV), fp32 softmax",
         "data": "synthetic", "config": workload_config(name, args.scaling, world),
         # our kernels per step (sage2_api.cu launch_prepare + the attention kernel): k_kv_stats, k_q_quant,
-        # Delta S, k_kv_quant (two launches, K and V halves, for N <= 2048), attention
-        "gpu_launches": (6 if N <= 2048 else 5) * args.steps,
+        # Delta S, k_kv_quant (two launches: K and V halves), attention
+        "gpu_launches": 6 * args.steps,
         "roofline": {"bound": "tensor", "kernel": f"k_attn{kver} (tcgen05 attention, v{kver})", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src, "kernel_ms": kms_max,

@@ -145,7 +145,7 @@ int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offse
  * k_bar and gamma(K), q_bar_i and gamma(Q_i), Delta S_i = q_bar_i gamma(K)^T
  * (P:193), per-thread INT4 groups of Q / K (INT8 with SAGE2_F_INT8), per-channel
  * E4M3 V; fills the workspace regions listed above.  Stream-ordered on `stream`: the Q
- * quantizer (and, for N <= 2048, Delta S and the K half of the K/V quantizer) run on library-owned side
+ * quantizer, the K half of the K/V quantizer and (for N <= 2048) Delta S run on library-owned side
  * streams of the device, forked from `stream` and joined back through events recorded per call, so the call behaves
  * as if it ran entirely on `stream` (also under CUDA graph capture of `stream`; tests/test_gpu_streams.py).
  * Errors: SAGE2_EINVAL (shape, flags, pointer / workspace size or alignment), SAGE2_EUNSUPPORTED,

@@ -264,6 +264,10 @@ int kernel_of(int N, int d, int flags) {
     return 8;
 }
 
+#ifndef SAGE2_KV_SPLIT_MAX_N
+#define SAGE2_KV_SPLIT_MAX_N (1 << 30)   // k_kv_quant as concurrent K / V launches (every N: DESIGN.md section 9)
+#endif
+
 template <int D>
 int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int Hq, int Hkv, int N, int flags,
                    uint8_t* ws, const Layout& L, cudaStream_t st) {
@@ -352,19 +356,21 @@ int launch_prepare(const __half* q, const __half* k, const __half* v, int B, int
     // persistent tensor-core GEMM (one 197 KB CTA per SM) loses its SMs to k_kv_quant when the two run
     // together (4K 343 -> 352 us, 32K 3.24 -> 3.44 ms), so it runs after the join
     const bool ds_side = side && ((flags & SAGE2_F_DS_SIMT) || N <= 2048);
-    // short sequences also split k_kv_quant into its K and V halves on two streams (a second side
-    // stream takes the K half), each CTA's serial load / reduce / quantize phases halved
-    cudaStream_t side2 = ds_side ? side_stream(1) : nullptr;
+    // k_kv_quant split into its K and V halves on two streams (a second side stream takes the K half):
+    // each CTA's serial load / reduce / quantize phases halved (C2-1K 83 -> 81 us, 4K 343 -> 329,
+    // 32K 3.20 -> 3.08 ms)
+    cudaStream_t side2 = side && N <= SAGE2_KV_SPLIT_MAX_N ? side_stream(1) : nullptr;
     cudaEvent_t ev_join2 = nullptr;
     if (side2 && cudaEventCreateWithFlags(&ev_join2, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         ev_join2 = nullptr;
         side2 = nullptr;
     }
+    // the K column sums are complete here: both side launches below wait for this event
+    if ((ds_side || side2) && cudaEventRecord(ev_stats, st) != cudaSuccess) return cuda_rc();
     if (side) {
         if (ds_side) {
-            if (cudaEventRecord(ev_stats, st) != cudaSuccess || cudaStreamWaitEvent(side, ev_stats, 0) != cudaSuccess)
-                return cuda_rc();
+            if (cudaStreamWaitEvent(side, ev_stats, 0) != cudaSuccess) return cuda_rc();
             int rc2 = launch_ds(side);
             if (rc2) return rc2;
         }
