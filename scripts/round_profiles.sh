@@ -13,7 +13,7 @@ for cfg in c2_32k_d128 c2_4k_d128 c2_32k_d64; do
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attn8 -s 3 -c 1 -f -o /tmp/reps/${TAG}_prof_attn8_c2_32k_d128 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attn12 -s 3 -c 1 -f -o /tmp/reps/${TAG}_prof_attn12_c2_32k_d64 python bench.py --config c2_32k_d64 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none -k 'regex:k_kv_stats|k_kv_quant|k_q_quant|k_delta_s' -s 4 -c 4 -f -o /tmp/reps/${TAG}_prof_prep_c2_32k_d128 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none -k 'regex:k_kv_stats|k_kv_quant|k_q_quant|k_delta_s' -s 5 -c 5 -f -o /tmp/reps/${TAG}_prof_prep_c2_32k_d128 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 # summaries only (the .ncu-rep files stay on the box: gpurun returns <= 64 MiB)
 python scripts/ncu_summary.py /tmp/reps/${TAG}_prof_attn8_c2_32k_d128.ncu-rep gpurun_out/${TAG}_launches_c2_32k_d128.csv c2_32k_d128 ${TAG} > gpurun_out/${TAG}_summary_32k.txt 2>&1
 python scripts/ncu_summary.py /tmp/reps/${TAG}_prof_attn12_c2_32k_d64.ncu-rep gpurun_out/${TAG}_launches_c2_32k_d64.csv c2_32k_d64 ${TAG} > gpurun_out/${TAG}_summary_32k_d64.txt 2>&1
