@@ -64,10 +64,6 @@ extern "C" {
 #define SAGE2_F_KERNEL_V12 131072 /* force the v12 kernel (csrc/attn12.cuh, d = 64 only: four Q tiles per  */
                                   /* CTA, b_kv = 64 -- the oracle's kv_tile is then 64, reading C-9).      */
                                   /* Not with QK_E4M3 / GRAN flags.                                       */
-#define SAGE2_F_KERNEL_V14 4194304 /* force the v14 kernel (csrc/attn14.cuh: one Q tile per CTA, S double- */
-                                  /* buffered, KV tiles alternating over two softmax pairs, promotion in  */
-                                  /* a correction warpgroup; b_kv = 128).  Non-causal; not with GRAN /     */
-                                  /* ONE_LEVEL flags.                                                     */
 #define SAGE2_F_ONE_LEVEL 1048576 /* ablation of the two-level accumulation (Table): the  */
                                   /* PV MMA accumulates into O in TMEM (O rescaled in place where the row */
                                   /* max moved); kernel v8 only.  Not the SageAttn2 default.              */
@@ -153,8 +149,7 @@ int sage2_workspace_layout(int B, int H_q, int H_kv, int N, int d, size_t* offse
 int sage2_prepare(const void* q, const void* k, const void* v, int B, int H_q, int H_kv, int N, int d,
                   int flags, void* workspace, size_t ws_bytes, void* stream);
 
-/* Which attention kernel sage2_attention runs for (N, d, flags): 14, 12 or 8 (SAGE2_F_KERNEL_V14 /
- * _V12 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
+/* Which attention kernel sage2_attention runs for (N, d, flags): 12 or 8 (SAGE2_F_KERNEL_V12 / _V8; ONE_LEVEL implies 8; with no selector and no QK_E4M3 / GRAN flag: 12 for d = 64
  * non-causal, 8 otherwise -- v8 runs one Q tile per CTA, two CTAs per SM, for N <= 1024).  Host-only,
  * no CUDA call; never fails. */
 int sage2_attention_kernel(int N, int d, int flags);

@@ -15,6 +15,11 @@ extern "C" {
 #endif
 
 #define SAGE2_F_DEBUG_TIMING 64 /* internal: clock64 phase-stamp builds of the attention kernels */
+/* Experimental attention kernel v14 (csrc/attn14.cuh), dev library only: one Q
+ * tile per CTA, S double-buffered in TMEM, KV tiles alternating over two softmax pairs, promotion in a
+ * correction warpgroup; b_kv = 128.  Measured slower than v8.  Accepted by sage2_prepare /
+ * sage2_attention / sage2_attention_kernel of libsage2_dev.so; non-causal; not with GRAN / ONE_LEVEL. */
+#define SAGE2_F_KERNEL_V14 4194304
 
 /* clock64 phase trace of the attention kernel sage2_attention would run (non-causal; a KERNEL flag
  * selects v8 / v12): stamps of CTA (0,0,0) written to `stamps` (device, caller-owned, zeroed,

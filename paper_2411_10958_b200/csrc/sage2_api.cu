@@ -20,7 +20,9 @@
 
 #include "../../include/sage2.h"
 #include "attn12.cuh"
-#include "attn14.cuh"
+#ifdef SAGE2_DEV
+#include "attn14.cuh"   // experimental kernel: dev library only
+#endif
 #include "attn8.cuh"
 #include "dsg.cuh"
 #include "prep.cuh"
@@ -195,7 +197,11 @@ cudaError_t lib_malloc_async(void** ptr, size_t bytes, cudaStream_t st) {
     return pool ? cudaMallocFromPoolAsync(ptr, bytes, pool, st) : cudaMallocAsync(ptr, bytes, st);
 }
 
-constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12 | SAGE2_F_KERNEL_V14;
+constexpr int kKernelFlags = SAGE2_F_KERNEL_V8 | SAGE2_F_KERNEL_V12
+#ifdef SAGE2_DEV
+                             | SAGE2_F_KERNEL_V14
+#endif
+    ;
 
 // Kernel launch with programmatic dependent launch (PDL): the kernel may start launching while the
 // previous kernel on the stream drains; every kernel of the library waits for its predecessor grid
@@ -236,7 +242,9 @@ bool flags_ok(int flags) {
     if ((flags & kGranFlags) && (flags & SAGE2_F_KERNEL_V12)) return false;
     if ((flags & SAGE2_F_QK_E4M3) && (flags & SAGE2_F_KERNEL_V12)) return false;
     // v14: non-causal, two-level, per-thread granularity
+#ifdef SAGE2_DEV
     if ((flags & SAGE2_F_KERNEL_V14) && (flags & (kGranFlags | SAGE2_F_ONE_LEVEL | SAGE2_F_CAUSAL))) return false;
+#endif
     const int granf = kGranFlags;
     if ((flags & granf) & ((flags & granf) - 1)) return false;     // at most one granularity
     if ((flags & SAGE2_F_GRAN_TENSOR) && (flags & SAGE2_F_SMOOTH_V)) return false;   // shares vsum
@@ -253,7 +261,9 @@ bool flags_ok(int flags) {
 // kernel fixes the order of the keys inside the V^T tile images and Delta S rows).
 int kernel_of(int N, int d, int flags) {
     if (flags & SAGE2_F_KERNEL_V12) return 12;
+#ifdef SAGE2_DEV
     if (flags & SAGE2_F_KERNEL_V14) return 14;
+#endif
     if (flags & (SAGE2_F_KERNEL_V8 | SAGE2_F_ONE_LEVEL)) return 8;
     // no selector: d = 64 non-causal -> v12 (four Q tiles per CTA, b_kv = 64: C2-32K 686 vs 665 TOPS,
     // C2-4K 643 vs 610, C2-1K 457 vs 434); v8 elsewhere.  (The persistent v10 of round 1 lost
@@ -439,6 +449,7 @@ int launch_attn12_t(const AttnParams& p, int B, cudaStream_t st) {
     return cuda_rc();
 }
 
+#ifdef SAGE2_DEV
 #ifndef SAGE2_V14_CORR
 #define SAGE2_V14_CORR 1   // correction warpgroup (16-column chunks): 1132 vs 1086 TOPS in-pair
 #endif
@@ -451,6 +462,7 @@ int launch_attn14_t(const AttnParams& p, int B, cudaStream_t st) {
     launch_k(k_attn14<D, QKF8, TIMING, CORR>, dim3(p.nT, p.Hq, B), dim3(CORR ? 768 : 640), smem, st, p);
     return cuda_rc();
 }
+#endif
 
 template <int D>
 int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStream_t st) {
@@ -462,13 +474,15 @@ int launch_attention_d(const AttnParams& p, int B, int flags, bool dump, cudaStr
         if constexpr (D == 64) {
             if (kern == 12) return launch_attn12_t<false, false, true>(p, B, st);
         }
-        if (kern == 14) return launch_attn14_t<D, false, true>(p, B, st);
+        if (kern == 14) return launch_attn14_t<D, false, true>(p, B, st);   // (inside #ifdef SAGE2_DEV)
         return launch_attn8_t<D, false, false, false, true>(p, B, st);
     }
 #endif
+#ifdef SAGE2_DEV
     if (kern == 14 && !dump) {   // one Q tile per CTA, S double-buffered (DUMP builds: v8)
         return f8 ? launch_attn14_t<D, true>(p, B, st) : launch_attn14_t<D, false>(p, B, st);
     }
+#endif
     if (kern == 12) {     // four Q tiles per CTA, b_kv = 64: head dim 64 only
         if constexpr (D != 64) {
             return SAGE2_EINVAL;

@@ -81,6 +81,11 @@ def dev_lib():
     return _dev
 
 
+def _lib_for(kernel):
+    """The experimental v14 kernel lives in the dev library only (include/sage2_dev.h)."""
+    return dev_lib() if kernel == "v14" else lib()
+
+
 def _check(rc, L=None):
     if rc != 0:
         L = L or lib()
@@ -151,7 +156,7 @@ def attn(q, k, v, causal=False, int8=False, out=None, workspace=None, qk_e4m3=Fa
         return out
     if workspace is None:
         workspace = alloc_workspace(B, Hq, Hkv, N, d, q.device)
-    _check(lib().sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
+    _check(_lib_for(kernel).sage2_attn_ex(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, Hq, Hkv, N, d,
                                flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel], workspace.data_ptr(),
                                workspace.numel(), _stream()))
     return out
@@ -170,18 +175,18 @@ def prepare(q, k, v, workspace, causal=False, int8=False, ds_simt=False, qk_e4m3
     _check_inputs(q, k, v)
     B, Hq, Hkv, N, d = _shape(q, k)
     fl = flags(causal, int8, qk_e4m3, smooth_v, gran) | (DS_SIMT if ds_simt else 0) | KERNEL_FLAGS[kernel]
-    _check(lib().sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
+    _check(_lib_for(kernel).sage2_prepare(q.data_ptr(), k.data_ptr(), v.data_ptr(), B, Hq, Hkv, N, d, fl,
                                workspace.data_ptr(), workspace.numel(), _stream()))
 
 
-KERNEL_FLAGS = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576, "v14": 4194304}   # include/sage2.h SAGE2_F_KERNEL_*; "one": v8 single-level ablation
+KERNEL_FLAGS = {"default": 0, "v8": 4096, "v12": 131072, "one": 1048576, "v14": 4194304}   # SAGE2_F_KERNEL_* (v14: sage2_dev.h, dev library); "one": v8 single-level ablation
 
 
 def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel="default", qk_e4m3=False,
               smooth_v=False, gran="thread"):
     """The tcgen05 attention kernel only, on a prepared workspace (kernel: "default" = the dispatch
     rule of sage2_attention_kernel, or "v8" / "v12" / "one"; data flags must match the prepare() call)."""
-    _check(lib().sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
+    _check(_lib_for(kernel).sage2_attention(out.data_ptr(), B, Hq, Hkv, N, d,
                                  flags(causal, int8, qk_e4m3, smooth_v, gran) | KERNEL_FLAGS[kernel],
                                  workspace.data_ptr(), workspace.numel(), _stream()))
     return out
@@ -189,7 +194,7 @@ def attention(out, workspace, B, Hq, Hkv, N, d, causal=False, int8=False, kernel
 
 def attention_kernel(N, d, causal=False, kernel="default", qk_e4m3=False, gran="thread"):
     """Version number of the attention kernel sage2_attention runs for these arguments (host only)."""
-    return int(lib().sage2_attention_kernel(N, d, flags(causal, False, qk_e4m3, False, gran) | KERNEL_FLAGS[kernel]))
+    return int(_lib_for(kernel).sage2_attention_kernel(N, d, flags(causal, False, qk_e4m3, False, gran) | KERNEL_FLAGS[kernel]))
 
 
 def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, qk_e4m3=False, kernel="default",
@@ -200,7 +205,7 @@ def debug_qk_int32(out, workspace, B, Hq, Hkv, N, d, int8=False, with_p=False, q
     Np = (N + 127) // 128 * 128
     s = torch.zeros((B * Hq, Np, Np), dtype=torch.int32, device=out.device)
     ph = torch.zeros((B * Hq, Np, Np), dtype=torch.uint8, device=out.device) if with_p else None
-    _check(lib().sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
+    _check(_lib_for(kernel).sage2_debug_qk_int32(out.data_ptr(), s.data_ptr(), ph.data_ptr() if with_p else None, B, Hq, Hkv,
                                       N, d, flags(False, int8, qk_e4m3, smooth_v) | KERNEL_FLAGS[kernel], workspace.data_ptr(), workspace.numel(),
                                       _stream()))
     return (s, ph) if with_p else s

@@ -31,7 +31,7 @@ ops = 4.0 * B * H * N * N * d
 libs, wss, variants = {}, {}, []
 for nm in names:
     base, _, lib = nm.partition("@")
-    lib = lib or sage2.LIB_PATH
+    lib = lib or (sage2.DEV_LIB_PATH if base.startswith("v14") else sage2.LIB_PATH)   # v14: dev library only
     if lib not in libs:
         libs[lib] = sage2._declare(ctypes.CDLL(lib))
     parts = base.split("_")
